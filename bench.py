@@ -1,0 +1,495 @@
+#!/usr/bin/env python
+"""Benchmark of the forward 2-D CDF 5/3 DWT (non-separable lifting) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+
+One "step" is one pass of the whole hot path over one batch of the workload:
+every level of the forward transform of the config's image(s) (and, for row
+strips at N > 1, the ghost-row exchange).  Default workload: BASELINE.json
+config 3 (16384 x 16384 fp32, 1 level), the configuration the north-star
+target ("70 % of HBM bandwidth per level on 16384 x 16384 fp32") is stated on;
+at N > 1 it is split into N row strips with an NCCL halo exchange (strong
+scaling: the image is fixed).  Inputs are 1 GiB, larger than the 126 MB L2,
+so no L2 flush is needed between steps.
+
+Timing: W untimed warm-up steps, then exactly K steps bracketed by a barrier
+and torch.cuda.synchronize() on both sides, CUDA events on the launching
+stream, max over ranks.  Rank 0 prints one JSON line.
+
+``--impl reference`` times the CPU oracle (oracle/, plain fp64 C) on the
+host cores instead: each step is a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "forward 2-D CDF 5/3 DWT Gpixel/s and HBM GB/s vs peak, 1/2/4/8 B200"
+UNIT = "Gpixel/s"
+BYTES_PER_PX = 8            # algorithmic: 4 B read + 4 B written per pixel per level
+FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="3", choices=["1", "2", "3", "4", "4b", "5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-overlap", action="store_true", help="strips: exchange, then one launch")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-rows", type=int, default=0, help="oracle sample rows (0 = auto)")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ----------------------------------------------------------------------------
+# clocks (NVML polled from a thread during the timed region)
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {"gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+               "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+               "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+               "display_clock_setting": 0x100}
+
+    def __init__(self, device_index: int):
+        self.samples = []
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = repr(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nvml
+        while not self._stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.perf_counter(), mhz, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self, t0, t1):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "nvml unavailable"}
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        window = "timed region"
+        if not inside:   # region shorter than the poll period: nearest samples
+            inside = sorted(self.samples, key=lambda s: min(abs(s[0] - t0), abs(s[0] - t1)))[:3]
+            window = "adjacent to timed region"
+        reasons = set()
+        for _, _, rs in inside:
+            for name, bit in self.REASONS.items():
+                if rs & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median([s[1] for s in inside]) if inside else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons), "samples": len(inside),
+                "window": window}
+
+
+# ----------------------------------------------------------------------------
+# workload
+# ----------------------------------------------------------------------------
+def describe(cfg, world):
+    g0 = cfg.groups[0]
+    if cfg.name == "5":
+        images = "256x2048^2 + 32x4095x3001"
+    else:
+        images = f"{g0.width}x{g0.height}"
+    return {"workload": f"config {cfg.name}: {cfg.description}", "images": images, "levels": cfg.levels,
+            "pixels": cfg.pixels, "input": "fp32, seeded synthetic, resident in HBM",
+            "l2": "inputs larger than the 126 MB L2; no flush between steps" if cfg.pixels * 4 > 126e6
+            else "L2 flushed (256 MB write) before every timed step",
+            "parallelism": ("row strips x%d, NCCL halo exchange" % world if cfg.name in ("1", "2", "3", "4", "4b")
+                            and world > 1 else ("image shards x%d, no communication" % world if world > 1
+                                                else "single GPU"))}
+
+
+class OursRunner:
+    """Device-resident inputs; step() enqueues one full forward on the current stream."""
+
+    def __init__(self, cfg, rank, world, device):
+        import torch
+        from paper_1708_07853_b200 import dwt2
+        from paper_1708_07853_b200 import distributed as D
+        self.cfg, self.rank, self.world = cfg, rank, world
+        self.dwt2, self.D = dwt2, D
+        self.torch = torch
+        self.flush = None
+        if cfg.pixels * 4 <= 126e6:
+            self.flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)   # 256 MB
+        self.launches = 0
+        self.algo_bytes = 0           # algorithmic bytes one step moves on this rank
+        self.level1_bytes = 0
+        self.pixels = 0               # finest-level pixels this rank transforms per step
+        self.h2d = self.d2h = 0
+        if cfg.name == "5":
+            self.items = []
+            for grp in cfg.groups:
+                idx = D.shard(grp.count, rank, world)
+                if len(idx) == 0:
+                    continue
+                xs = np.stack([grp.image(i) for i in idx])
+                x = torch.from_numpy(xs).to(device)
+                out = torch.empty_like(x)
+                plan = dwt2.Plan(grp.width, grp.height, cfg.levels, max_count=len(idx))
+                info = plan.info()
+                self.items.append((plan, x, out))
+                self.launches += info.launches_per_forward
+                self.algo_bytes += info.algorithmic_bytes * len(idx)
+                self.level1_bytes += BYTES_PER_PX * grp.width * grp.height * len(idx)
+                self.pixels += grp.width * grp.height * len(idx)
+            self.mode = "batch"
+        elif world == 1:
+            g = cfg.groups[0]
+            x = torch.from_numpy(g.image(0)).to(device)
+            self.x, self.out = x, torch.empty_like(x)
+            self.plan = dwt2.Plan(g.width, g.height, cfg.levels)
+            info = self.plan.info()
+            self.launches = info.launches_per_forward
+            self.algo_bytes = info.algorithmic_bytes
+            self.level1_bytes = BYTES_PER_PX * g.width * g.height
+            self.pixels = g.width * g.height
+            self.mode = "single"
+            self.host_img = g.image(0)
+        else:
+            if cfg.levels != 1:
+                raise SystemExit("row strips are one-level (multi-level strips: SURVEY 8f N3)")
+            g = cfg.groups[0]
+            img = g.image(0)
+            self.ex = D.StripExchange(g.width, g.height, rank, world, device=device)
+            r0, r1 = self.ex.r0, self.ex.r1
+            self.ex.buf.copy_(torch.from_numpy(np.ascontiguousarray(
+                img[r0 - self.ex.ghost_top:r1 + self.ex.ghost_bot])))
+            self.splan = dwt2.StripPlan(g.width, g.height, r0, r1)
+            self.out = torch.empty((r1 - r0, g.width), dtype=torch.float32, device=device)
+            self.launches = 1 if self.overlap_off else 2
+            self.algo_bytes = BYTES_PER_PX * g.width * (r1 - r0)
+            self.level1_bytes = self.algo_bytes
+            self.pixels = g.width * (r1 - r0)
+            self.mode = "strip"
+            self.host_img = img
+
+    overlap_off = False
+
+    def step(self):
+        if self.flush is not None:
+            self.flush.zero_()
+        if self.mode == "single":
+            self.plan.forward(self.x, self.out)
+        elif self.mode == "batch":
+            for plan, x, out in self.items:
+                plan.forward(x, out)
+        else:
+            self.D.strip_forward_step(self.ex, self.splan, self.out, overlap=not self.overlap_off)
+
+    def level1_kernel_ms(self, iters):
+        """Average duration of the dominant kernel (level 1), CUDA events on its stream."""
+        torch = self.torch
+        s = torch.cuda.current_stream()
+        if self.mode == "single" and self.cfg.levels == 1:
+            return None   # identical to the step: caller uses the step time
+        if self.mode == "strip":
+            return None
+        # time level-1-only plans on the same buffers
+        ts = []
+        for _ in range(iters):
+            if self.flush is not None:
+                self.flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            if self.mode == "single":
+                self._l1plan = getattr(self, "_l1plan", None) or self.dwt2.Plan(self.cfg.groups[0].width,
+                                                                                self.cfg.groups[0].height, 1)
+                self._l1plan.forward(self.x, self.out)
+            else:
+                if not hasattr(self, "_l1items"):
+                    self._l1items = [(self.dwt2.Plan(p.width, p.height, 1, max_count=x.shape[0]), x, o)
+                                     for p, x, o in self.items]
+                for p, x, o in self._l1items:
+                    p.forward(x, o)
+            e1.record(s)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return sum(ts) / len(ts)
+
+    def e2e(self, steps, warm):
+        """Same metric through the public API with HOST buffers: H2D of the
+        step's input from pinned memory and D2H of its result are inside the
+        timed region (the C-ABI dwt2_forward_host pipelines them by row band)."""
+        torch = self.torch
+        if self.mode == "single":
+            hin = torch.from_numpy(self.host_img).pin_memory()
+            hout = torch.empty_like(hin).pin_memory()
+            for _ in range(warm):
+                self.plan.forward_host(hin, hout)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                self.plan.forward_host(hin, hout)
+            dt = (time.perf_counter() - t0) / steps
+            self.h2d = self.d2h = hin.numel() * 4
+            return dt
+        if self.mode == "strip":
+            hin = torch.from_numpy(np.ascontiguousarray(self.ex.strip.cpu().numpy())).pin_memory()
+            hout = torch.empty(self.out.shape, dtype=torch.float32).pin_memory()
+            s = torch.cuda.current_stream()
+            def one():
+                self.ex.strip.copy_(hin, non_blocking=True)
+                self.D.strip_forward_step(self.ex, self.splan, self.out, overlap=True)
+                hout.copy_(self.out, non_blocking=True)
+            for _ in range(warm):
+                one()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(steps):
+                one()
+            e1.record(s)
+            e1.synchronize()
+            self.h2d, self.d2h = hin.numel() * 4, hout.numel() * 4
+            return e0.elapsed_time(e1) / 1e3 / steps
+        # batch: per group H2D -> batched forward -> D2H
+        hosts = [(torch.empty(x.shape, dtype=torch.float32).pin_memory(),
+                  torch.empty(x.shape, dtype=torch.float32).pin_memory()) for _, x, _ in self.items]
+        for (hi, _), (_, x, _) in zip(hosts, self.items):
+            hi.copy_(x.cpu())
+        s = torch.cuda.current_stream()
+
+        def one():
+            for (hi, ho), (plan, x, o) in zip(hosts, self.items):
+                x.copy_(hi, non_blocking=True)
+                plan.forward(x, o)
+                ho.copy_(o, non_blocking=True)
+        for _ in range(warm):
+            one()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(steps):
+            one()
+        e1.record(s)
+        e1.synchronize()
+        self.h2d = sum(h.numel() * 4 for h, _ in hosts)
+        self.d2h = self.h2d
+        return e0.elapsed_time(e1) / 1e3 / steps
+
+
+def oracle_sample(cfg, budget_s: float, rows: int = 0):
+    """Bounded sample of the workload for the CPU oracle: a full-width band of
+    the first image (or whole images for config 5), transformed as a
+    standalone image with the config's levels.  Returns (fn, pixels, text)."""
+    import oracle
+    g = cfg.groups[0]
+    if rows <= 0:
+        # ~0.1 us/pixel/level-ish single thread: size for ~budget_s
+        rows = int(max(64, min(g.height, budget_s / 1.1e-7 / g.width)))
+        rows -= rows % 2
+    img = g.image(0)[:rows]
+    x64 = img.astype(np.float64)
+    lv = min(cfg.levels, 30)
+    # every level must stay >= 2 x 2
+    w, h, L = g.width, rows, 0
+    while L < lv and w >= 2 and h >= 2:
+        w, h, L = (w + 1) // 2, (h + 1) // 2, L + 1
+
+    def fn():
+        oracle.forward(x64, L, round_f32=True)
+    return fn, g.width * rows, f"{g.width}x{rows} band of image 0 of config {cfg.name}, {L} level(s), oracle algorithm A (separable lifting, fp64), 1 thread"
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def ncu_traffic(cfg_name):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        e = d.get("configs", {}).get(cfg_name)
+        return None if e is None else e.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    per_step_budget = 0.5
+    fn, px, text = oracle_sample(cfg, per_step_budget, args.cpu_sample_rows)
+    for _ in range(args.warmup):
+        fn()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fn()
+    dt = (time.perf_counter() - t0) / args.steps
+    v = px / dt / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "strong" if cfg.name != "5" else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": describe(cfg, 1),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": text},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    from paper_1708_07853_b200 import workloads
+    cfg = workloads.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world if world > 1 else args.gpus
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+
+    OursRunner.overlap_off = args.no_overlap
+    runner = OursRunner(cfg, rank, world, device)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        runner.step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.05)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_host0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        runner.step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_host1 = time.perf_counter()
+    barrier()
+    sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if runner.flush is not None:
+        # subtract the L2-flush kernel, timed alone
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            runner.flush.zero_()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ms -= f0.elapsed_time(f1) / args.steps
+    ms_t = torch.tensor([ms], device=device)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    total_px = cfg.pixels
+    value = total_px / (ms_max * 1e-3) / 1e9
+
+    # dominant kernel (level 1) duration
+    k_ms = runner.level1_kernel_ms(max(3, args.steps))
+    if k_ms is None:
+        k_ms = ms / max(1, (runner.launches if runner.mode != "strip" else 1))
+    k_bytes = runner.level1_bytes
+    achieved = k_bytes / (k_ms * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+    traffic = ncu_traffic(cfg.name) if world == 1 else None
+
+    # end to end through the host-buffer API
+    e2e = None
+    if not args.no_e2e:
+        e_steps = max(1, min(args.steps, 10))
+        dt = runner.e2e(e_steps, 1)
+        dt_t = torch.tensor([dt], device=device)
+        if world > 1:
+            dist.all_reduce(dt_t, op=dist.ReduceOp.MAX)
+        e2e = {"value": total_px / float(dt_t.item()) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(runner.h2d) * world, "d2h_bytes_per_step": int(runner.d2h) * world}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        fn, px, text = oracle_sample(cfg, 10.0, args.cpu_sample_rows)
+        t0 = time.perf_counter()
+        fn()
+        dt = time.perf_counter() - t0
+        cpu = {"value": px / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": text}
+
+    if rank == 0:
+        clocks = sampler.summary(t_host0, t_host1)
+        algo_bytes_total = runner.algo_bytes * world if cfg.name != "5" else sum(
+            BYTES_PER_PX * workloads.level_pixels(g.width, g.height, cfg.levels) * g.count for g in cfg.groups)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak" if cfg.name == "5" else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": describe(cfg, world),
+            "hbm_gbs_algorithmic": algo_bytes_total / (ms_max * 1e-3) / 1e9,
+            "ns_per_pel": ms_max * 1e6 / total_px,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "dwt53_level_kernel (level 1)", "kernel_ms": k_ms,
+                         "bytes_per_launch": k_bytes, "peak_source": peak_src,
+                         "frac_of_8tbs": achieved / 8000.0},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": runner.launches * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,160 @@
+/*
+ * dwt2.h -- C ABI of the B200-native forward 2-D CDF 5/3 DWT computed with
+ * the non-separable lifting scheme of arXiv:1708.07853.
+ *
+ * Operation (section 3, Eq. (5)): one decomposition level
+ * maps every 2x2 quad (a, b, c, d) = (x[2n][2m], x[2n][2m+1], x[2n+1][2m],
+ * x[2n+1][2m+1]) to the four subband coefficients (LL, HL, LH, HH) by a
+ * spatial predict followed by a spatial update,
+ *
+ *   predict  [1 0 0 0; P 1 0 0; P* 0 1 0; PP* P* P 1]
+ *   update   [1 U U* UU*; 0 1 0 U*; 0 0 1 U; 0 0 0 1]
+ *
+ * with the CDF 5/3 lifting pair P = -1/2 (1 + z), U = 1/4 (1 + z^-1)
+ * (coefficients SPEC.md L145).  In exact arithmetic the result
+ * is the separable 2-D CDF 5/3 transform (tensor product of
+ * 1-D transforms).  Boundaries: whole-sample symmetric extension (the paper
+ * is silent).  Multi-level: the transform recurses on LL,
+ * W_{k+1} = ceil(W_k / 2), H_{k+1} = ceil(H_k / 2) (BASELINE.json north_star).
+ *
+ * Layouts.  Images are fp32, row-major.  The output is the Mallat pyramid
+ * (SPEC.md L358-366): level k writes, inside the W x H output with the
+ * caller's row pitch,
+ *     HL_k -> rows [0, ceil(H_k/2)),   cols [ceil(W_k/2), W_k)
+ *     LH_k -> rows [ceil(H_k/2), H_k), cols [0, ceil(W_k/2))
+ *     HH_k -> rows [ceil(H_k/2), H_k), cols [ceil(W_k/2), W_k)
+ * and the last level's LL goes to rows [0, ceil(H_L/2)), cols
+ * [0, ceil(W_L/2)).  HL is the horizontal high band (odd column, even row).
+ *
+ * Arithmetic: fp32 in HBM, fp64 in registers.  For
+ * integer-valued inputs in [0, 255] the result is bit-exact at every level
+ * that fits the fp32 mantissa (levels 1-2); otherwise every level's output is
+ * the correctly rounded fp32 value of the exact level result.
+ *
+ * Execution: every call is asynchronous on the given CUDA stream (pass a
+ * cudaStream_t; NULL = legacy default stream).  No host synchronisation, no
+ * device allocation and no retained pointers inside dwt2_forward*, except
+ * dwt2_forward_host (see there).  Concurrent calls that share one plan must
+ * be serialised by the caller (the plan owns its LL scratch); distinct plans
+ * are independent.  A plan is bound to the CUDA device current at creation.
+ *
+ * Errors: functions returning int32_t return DWT2_OK (0) or a negative code;
+ * plan constructors return NULL and set a thread-local code readable with
+ * dwt2_last_error().  Asynchronous kernel faults surface at the caller's next
+ * synchronisation, as for any CUDA launch.
+ */
+#ifndef DWT2_H
+#define DWT2_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Opaque CUDA stream handle, ABI-identical to cudaStream_t. */
+typedef struct CUstream_st *dwt2_stream_t;
+
+typedef struct dwt2_plan dwt2_plan;
+
+enum {
+    DWT2_OK = 0,
+    DWT2_EINVAL = -1,      /* bad argument: null, overlap, size, alignment, wrong device */
+    DWT2_ENOMEM = -2,      /* device or pinned host allocation failed */
+    DWT2_ECUDA = -3,       /* a CUDA runtime / driver call or a launch failed */
+    DWT2_EUNSUPPORTED = -4 /* boundary mode other than SYMMETRIC, or device is not sm_100 */
+};
+
+enum { DWT2_BOUNDARY_SYMMETRIC = 0 }; /* whole-sample symmetric extension */
+
+enum {                         /* dwt2_forward_strip `part` */
+    DWT2_STRIP_ALL = 0,        /* every quad row of the strip */
+    DWT2_STRIP_INTERIOR = 1,   /* quad rows that read no ghost row */
+    DWT2_STRIP_BOUNDARY = 2    /* the first and the last quad row (read ghost rows) */
+};
+
+/* Plan for a single W x H image, `levels` levels (1 <= levels, and every
+ * level's input at least 2 x 2).  boundary must be DWT2_BOUNDARY_SYMMETRIC.
+ * Allocates and owns the LL scratch of levels >= 2 on the current device.
+ * Returns NULL on error (dwt2_last_error()). */
+dwt2_plan *dwt2_plan_create(int32_t width, int32_t height, int32_t levels, int32_t boundary);
+
+/* As dwt2_plan_create, with scratch for up to max_count images per
+ * dwt2_forward_batched call (BASELINE.json config 5). */
+dwt2_plan *dwt2_plan_create_batched(int32_t width, int32_t height, int32_t levels,
+                                    int32_t boundary, int32_t max_count);
+
+/* One-level plan for the row strip [row_begin, row_end) of a width x
+ * global_height image (the paper's row bands, SPEC.md
+ * L313-318).  row_begin must be even; row_end must be even or equal to
+ * global_height; 0 <= row_begin < row_end <= global_height.
+ * Input rows present in the `in` buffer of dwt2_forward_strip:
+ *   2 ghost rows above the strip if row_begin > 0 (rows row_begin-2, -1),
+ *   the strip rows, then 1 ghost row below if row_end < global_height.
+ * Output: the strip-local Mallat layout of W x (row_end - row_begin): the
+ * strip's quad rows of LL | HL over LH | HH. */
+dwt2_plan *dwt2_plan_create_strip(int32_t width, int32_t global_height, int32_t row_begin,
+                                  int32_t row_end, int32_t boundary);
+
+/* Forward transform of one image.
+ * in:  device pointer, W x H fp32, row pitch W elements, caller-owned,
+ *      read-only, 4-byte aligned.
+ * out: device pointer, W x H fp32 Mallat pyramid, row pitch W, caller-owned.
+ * in and out must not overlap (no in-place transform).
+ * Returns DWT2_OK, DWT2_EINVAL or DWT2_ECUDA. */
+int32_t dwt2_forward(const dwt2_plan *plan, const float *in, float *out, dwt2_stream_t stream);
+
+/* Forward transform of `count` images of the plan's size (count <= the
+ * plan's max_count).  Image i is read at in + i * in_stride and written at
+ * out + i * out_stride (element strides, >= W * H).  One launch per level
+ * covers all images. */
+int32_t dwt2_forward_batched(const dwt2_plan *plan, const float *in, float *out, int32_t count,
+                             int64_t in_stride, int64_t out_stride, dwt2_stream_t stream);
+
+/* Forward transform of a strip plan (see dwt2_plan_create_strip for the
+ * `in` / `out` layouts).  part selects all quad rows, only the interior ones
+ * (which read no ghost row, so they may run while the ghost rows are still in
+ * flight) or only the two boundary quad rows. */
+int32_t dwt2_forward_strip(const dwt2_plan *plan, const float *in, float *out, int32_t part,
+                           dwt2_stream_t stream);
+
+/* End-to-end call on HOST buffers: host_in (W x H fp32) is copied to the
+ * device, transformed, and the Mallat result copied back to host_out, all on
+ * `stream`; returns after the stream has drained (the only synchronising
+ * call).  The copies are chunked by row bands and overlapped with the level-1
+ * kernel (copy engine H2D || kernel || D2H).  Pinned (page-locked) host
+ * buffers are required for full speed; pageable buffers work but serialise.
+ * The first call allocates device staging (2 x W x H fp32) owned by the plan.
+ * Single-image plans only. */
+int32_t dwt2_forward_host(const dwt2_plan *plan, const float *host_in, float *host_out,
+                          dwt2_stream_t stream);
+
+/* Frees the plan and its device memory (cudaFree synchronises the device).
+ * NULL is a no-op.  No work using the plan may be in flight. */
+void dwt2_destroy(dwt2_plan *plan);
+
+/* Static facts of a plan, for benchmarks and tests. */
+typedef struct {
+    int32_t width, height, levels, max_count;
+    int32_t launches_per_forward;    /* kernel launches one dwt2_forward issues */
+    int32_t tma_levels;              /* levels served by the TMA-staged kernel */
+    int64_t algorithmic_bytes;       /* 8 B x sum_k W_k H_k (one image) */
+    int64_t scratch_bytes;           /* device bytes owned by the plan */
+} dwt2_plan_info_t;
+
+int32_t dwt2_plan_info(const dwt2_plan *plan, dwt2_plan_info_t *info);
+
+/* Thread-local code of the last failing call in this thread (0 if none). */
+int32_t dwt2_last_error(void);
+
+/* Static description of a code; never NULL. */
+const char *dwt2_error_string(int32_t code);
+
+/* Library version string, e.g. "dwt2-b200 0.1 sm_100a". */
+const char *dwt2_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DWT2_H */

@@ -1,0 +1,240 @@
+"""Thin Python binding of the C ABI in include/dwt2.h (argument marshalling only).
+
+Every function here forwards to libdwt2.so; every step of the transform runs
+in the CUDA kernels behind it.  There is no CPU fallback: if the library is
+missing or cannot be loaded, import-time use raises ``RuntimeError``.
+
+torch is used only for device memory and streams (tensors' data pointers and
+``torch.cuda.current_stream().cuda_stream``), as BASELINE.json north_star says.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdwt2.so")
+
+DWT2_OK, DWT2_EINVAL, DWT2_ENOMEM, DWT2_ECUDA, DWT2_EUNSUPPORTED = 0, -1, -2, -3, -4
+DWT2_BOUNDARY_SYMMETRIC = 0
+DWT2_STRIP_ALL, DWT2_STRIP_INTERIOR, DWT2_STRIP_BOUNDARY = 0, 1, 2
+
+# symbol -> (restype, argtypes); mirrors include/dwt2.h exactly
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("width", _I32), ("height", _I32), ("levels", _I32), ("max_count", _I32),
+                ("launches_per_forward", _I32), ("tma_levels", _I32),
+                ("algorithmic_bytes", _I64), ("scratch_bytes", _I64)]
+
+
+SIGNATURES = {
+    "dwt2_plan_create": (_P, [_I32, _I32, _I32, _I32]),
+    "dwt2_plan_create_batched": (_P, [_I32, _I32, _I32, _I32, _I32]),
+    "dwt2_plan_create_strip": (_P, [_I32, _I32, _I32, _I32, _I32]),
+    "dwt2_forward": (_I32, [_P, _P, _P, _P]),
+    "dwt2_forward_batched": (_I32, [_P, _P, _P, _I32, _I64, _I64, _P]),
+    "dwt2_forward_strip": (_I32, [_P, _P, _P, _I32, _P]),
+    "dwt2_forward_host": (_I32, [_P, _P, _P, _P]),
+    "dwt2_destroy": (None, [_P]),
+    "dwt2_plan_info": (_I32, [_P, ctypes.POINTER(PlanInfo)]),
+    "dwt2_last_error": (_I32, []),
+    "dwt2_error_string": (ctypes.c_char_p, [_I32]),
+    "dwt2_version": (ctypes.c_char_p, []),
+}
+
+_lib = None
+
+
+class DWT2Error(RuntimeError):
+    def __init__(self, code: int, what: str):
+        self.code = code
+        super().__init__(f"{what}: {error_string(code)} ({code})")
+
+
+def lib() -> ctypes.CDLL:
+    """Load libdwt2.so (in-tree).  Raises if it is absent: no fallback path."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                               "(nvcc for sm_100a); there is no CPU fallback")
+        l = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(l, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = l
+    return _lib
+
+
+def error_string(code: int) -> str:
+    return lib().dwt2_error_string(code).decode()
+
+
+def version() -> str:
+    return lib().dwt2_version().decode()
+
+
+def _check(code: int, what: str) -> None:
+    if code != DWT2_OK:
+        raise DWT2Error(code, what)
+
+
+def _plan_or_raise(ptr, what):
+    if not ptr:
+        raise DWT2Error(lib().dwt2_last_error(), what)
+    return ptr
+
+
+# ---- raw C-ABI names (pointers are ints) -------------------------------------
+
+def dwt2_plan_create(width, height, levels, boundary=DWT2_BOUNDARY_SYMMETRIC):
+    return _plan_or_raise(lib().dwt2_plan_create(width, height, levels, boundary), "dwt2_plan_create")
+
+
+def dwt2_plan_create_batched(width, height, levels, boundary, max_count):
+    return _plan_or_raise(lib().dwt2_plan_create_batched(width, height, levels, boundary, max_count),
+                          "dwt2_plan_create_batched")
+
+
+def dwt2_plan_create_strip(width, global_height, row_begin, row_end, boundary=DWT2_BOUNDARY_SYMMETRIC):
+    return _plan_or_raise(lib().dwt2_plan_create_strip(width, global_height, row_begin, row_end, boundary),
+                          "dwt2_plan_create_strip")
+
+
+def dwt2_forward(plan, in_ptr, out_ptr, stream):
+    _check(lib().dwt2_forward(plan, in_ptr, out_ptr, stream), "dwt2_forward")
+
+
+def dwt2_forward_batched(plan, in_ptr, out_ptr, count, in_stride, out_stride, stream):
+    _check(lib().dwt2_forward_batched(plan, in_ptr, out_ptr, count, in_stride, out_stride, stream),
+           "dwt2_forward_batched")
+
+
+def dwt2_forward_strip(plan, in_ptr, out_ptr, part, stream):
+    _check(lib().dwt2_forward_strip(plan, in_ptr, out_ptr, part, stream), "dwt2_forward_strip")
+
+
+def dwt2_forward_host(plan, host_in_ptr, host_out_ptr, stream):
+    _check(lib().dwt2_forward_host(plan, host_in_ptr, host_out_ptr, stream), "dwt2_forward_host")
+
+
+def dwt2_destroy(plan):
+    lib().dwt2_destroy(plan)
+
+
+def dwt2_plan_info(plan) -> PlanInfo:
+    info = PlanInfo()
+    _check(lib().dwt2_plan_info(plan, ctypes.byref(info)), "dwt2_plan_info")
+    return info
+
+
+# ---- torch-facing convenience (marshalling only) ------------------------------
+
+def _stream_handle(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _check_image(x, name):
+    import torch
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
+
+
+class Plan:
+    """Owns a dwt2_plan* (see include/dwt2.h)."""
+
+    def __init__(self, width: int, height: int, levels: int = 1, max_count: int = 1):
+        self.width, self.height, self.levels, self.max_count = width, height, levels, max_count
+        if max_count == 1:
+            self._p = dwt2_plan_create(width, height, levels)
+        else:
+            self._p = dwt2_plan_create_batched(width, height, levels, DWT2_BOUNDARY_SYMMETRIC, max_count)
+
+    @property
+    def handle(self):
+        return self._p
+
+    def info(self) -> PlanInfo:
+        return dwt2_plan_info(self._p)
+
+    def forward(self, x, out=None, stream=None):
+        _check_image(x, "x")
+        if tuple(x.shape[-2:]) != (self.height, self.width):
+            raise ValueError(f"expected (..., {self.height}, {self.width}), got {tuple(x.shape)}")
+        import torch
+        if out is None:
+            out = torch.empty_like(x)
+        _check_image(out, "out")
+        if x.dim() == 2:
+            dwt2_forward(self._p, x.data_ptr(), out.data_ptr(), _stream_handle(stream))
+        else:
+            n = x.numel() // (self.width * self.height)
+            img = self.width * self.height
+            dwt2_forward_batched(self._p, x.data_ptr(), out.data_ptr(), n, img, img, _stream_handle(stream))
+        return out
+
+    def forward_host(self, host_in, host_out, stream=None):
+        """host_in / host_out: CPU float32 tensors (pinned for full speed)."""
+        dwt2_forward_host(self._p, host_in.data_ptr(), host_out.data_ptr(), _stream_handle(stream))
+        return host_out
+
+    def close(self):
+        if getattr(self, "_p", None):
+            dwt2_destroy(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class StripPlan:
+    """One-level plan for the row strip [row_begin, row_end) of a W x Hg image."""
+
+    def __init__(self, width: int, global_height: int, row_begin: int, row_end: int):
+        self.width, self.global_height = width, global_height
+        self.row_begin, self.row_end = row_begin, row_end
+        self.ghost_top = 2 if row_begin > 0 else 0
+        self.ghost_bot = 1 if row_end < global_height else 0
+        self._p = dwt2_plan_create_strip(width, global_height, row_begin, row_end)
+
+    @property
+    def in_rows(self) -> int:
+        return self.row_end - self.row_begin + self.ghost_top + self.ghost_bot
+
+    def forward(self, x_with_ghosts, out, part=DWT2_STRIP_ALL, stream=None):
+        _check_image(x_with_ghosts, "x")
+        _check_image(out, "out")
+        dwt2_forward_strip(self._p, x_with_ghosts.data_ptr(), out.data_ptr(), part, _stream_handle(stream))
+        return out
+
+    def close(self):
+        if getattr(self, "_p", None):
+            dwt2_destroy(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def forward(x, levels: int = 1):
+    """One-shot forward DWT of a (H, W) or (N, H, W) CUDA float32 tensor."""
+    p = Plan(x.shape[-1], x.shape[-2], levels, max_count=max(1, x.numel() // (x.shape[-1] * x.shape[-2])))
+    try:
+        return p.forward(x)
+    finally:
+        import torch
+        torch.cuda.current_stream().synchronize()
+        p.close()

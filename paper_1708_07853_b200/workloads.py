@@ -115,19 +115,3 @@ def level_pixels(width: int, height: int, levels: int) -> int:
         total += w * h
         w, h = (w + 1) // 2, (h + 1) // 2
     return total
-
-
-def shard(count: int, rank: int, world: int) -> range:
-    """Contiguous balanced share of `count` items for `rank` of `world`."""
-    lo = (count * rank) // world
-    hi = (count * (rank + 1)) // world
-    return range(lo, hi)
-
-
-def strip_rows(height: int, rank: int, world: int) -> tuple:
-    """Balanced even-aligned row strip [r_g, r_{g+1}) of rank g:
-    r_g = 2 * floor(g * ceil(H/2) / G), last strip ends at H."""
-    hq = (height + 1) // 2
-    lo = 2 * ((rank * hq) // world)
-    hi = height if rank == world - 1 else 2 * (((rank + 1) * hq) // world)
-    return lo, hi

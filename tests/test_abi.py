@@ -1,0 +1,75 @@
+"""CPU-side checks of the C ABI: the library builds for sm_100a, loads, and
+exports every function include/dwt2.h declares (no compute call without a GPU)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_1708_07853_b200 import _build, dwt2
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "dwt2.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(dwt2_[a-z_]+)\s*\(", src)
+    return sorted(set(names))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    _build.build()
+    return dwt2.lib()
+
+
+def test_header_declares_expected_api():
+    names = declared_functions()
+    for n in ["dwt2_plan_create", "dwt2_forward", "dwt2_destroy", "dwt2_forward_batched",
+              "dwt2_plan_create_strip", "dwt2_forward_strip", "dwt2_forward_host", "dwt2_last_error",
+              "dwt2_error_string"]:
+        assert n in names
+
+
+def test_every_declared_symbol_exported(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", dwt2.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (dwt2_\w+)", out))
+    for name in declared_functions():
+        assert name in exported, name
+        assert hasattr(lib, name)
+    assert set(dwt2.SIGNATURES) == set(declared_functions())
+
+
+def test_library_is_sm100a(lib):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", dwt2.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", dwt2.LIB_PATH],
+                          capture_output=True, text=True).stdout
+    assert "UTMALDG" in sass          # TMA-staged tile loads
+    assert "SHFL" in sass             # warp-shuffle neighbour exchange
+    assert "DFMA" in sass             # fp64 register arithmetic
+
+
+def test_static_strings(lib):
+    assert "sm_100a" in dwt2.version()
+    assert dwt2.error_string(0) == "ok"
+    assert dwt2.error_string(dwt2.DWT2_EINVAL) == "invalid argument"
+    assert dwt2.error_string(12345) == "unknown error"
+
+
+def test_plan_info_struct_layout():
+    assert ctypes.sizeof(dwt2.PlanInfo) == 6 * 4 + 2 * 8
+
+
+def test_oracle_not_imported_by_product():
+    pkg = os.path.join(ROOT, "paper_1708_07853_b200")
+    for dp, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".h", ".cpp")):
+                txt = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "dwt53_oracle" not in txt, f
