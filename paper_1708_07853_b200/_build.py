@@ -23,6 +23,18 @@ NVCC_FLAGS = [
 ]
 
 
+def build_variant(name: str, defines: dict) -> str:
+    """Tuning builds (e.g. stages / warps per CTA) under build/variants/."""
+    out_dir = os.path.join(ROOT, "build", "variants")
+    os.makedirs(out_dir, exist_ok=True)
+    out = os.path.join(out_dir, f"libdwt2_{name}.so")
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{k}={v}" for k, v in defines.items()], SRC, "-o", out]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     stale = (not os.path.exists(LIB) or
              os.path.getmtime(LIB) < max(os.path.getmtime(SRC), os.path.getmtime(HDR)))

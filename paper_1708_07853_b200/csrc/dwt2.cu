@@ -43,6 +43,7 @@
 #include <cstring>
 #include <mutex>
 #include <new>
+#include <type_traits>
 
 #include "../../include/dwt2.h"
 
@@ -50,47 +51,108 @@ namespace {
 
 // ---------------------------------------------------------------------------
 // Tile geometry
+//
+// A warp owns a column slab of SLAB = 64 QPL pixels: lane l holds the 2 QPL
+// pixel columns starting at x0 + 2 QPL l, i.e. QPL quads.  Its smem ring
+// holds, per row, the slab plus the 5/3 halo (2 columns left, 1 right),
+// staged by NBOX 2-D TMA boxes of 136 x BOXH floats (a TMA box extent is at
+// most 256 elements; a 544-byte inner extent keeps every row 16-B aligned):
+//   QPL = 2: one box,  columns [x0 - 4, x0 + 132)
+//   QPL = 4: two boxes, columns [x0 - 8, x0 + 128) and [x0 + 128, x0 + 264)
 // ---------------------------------------------------------------------------
-constexpr int SLAB = 128;          // output pixel columns per warp (64 quads, 2 per lane)
-constexpr int BOXW = 136;          // smem row: pixel columns [x0 - 4, x0 + 132)
-constexpr int R = 16;              // rows per pipeline stage (one TMA box = BOXW x R)
-constexpr int S = 3;               // stages per warp ring
-constexpr int WARPS = 4;           // warps (adjacent slabs) per CTA
+#ifndef DWT2_QPL
+#define DWT2_QPL 2
+#endif
+#ifndef DWT2_PAIRS
+#define DWT2_PAIRS 8
+#endif
+#ifndef DWT2_STAGES
+#define DWT2_STAGES 3
+#endif
+#ifndef DWT2_WARPS
+#define DWT2_WARPS 4
+#endif
+#ifndef DWT2_MINB
+#define DWT2_MINB 1
+#endif
+#ifndef DWT2_L2_PROMOTION
+#define DWT2_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_NONE
+#endif
+constexpr int QPL = DWT2_QPL;               // quads per lane (2 or 4)
+constexpr int SLAB = 64 * QPL;              // output pixel columns per warp
+constexpr int NBOX = QPL / 2;               // TMA boxes per stage
+constexpr int BOXW = 136;                   // box inner extent (floats)
+constexpr int BOX0 = (QPL == 2) ? -4 : -8;  // column of box 0 relative to x0
+constexpr int BOX1 = 128;                   // column of box 1 relative to x0 (QPL = 4)
+constexpr int PAIRS = DWT2_PAIRS;           // row pairs (quad rows) per pipeline stage
+constexpr int ROWS = 2 * PAIRS;             // new rows per stage
+constexpr int BOXH = ROWS + 1;              // a stage holds rows [r, r + ROWS + 1): its first (even)
+                                            // row is also the last row of the previous stage, so
+                                            // an (odd, even) row pair never straddles two stages
+constexpr int S = DWT2_STAGES;              // stages per warp ring
+constexpr int WARPS = DWT2_WARPS;           // warps per CTA (independent; packing only)
 constexpr int THREADS = WARPS * 32;
-constexpr int GROUP = WARPS * SLAB;                      // pixel columns per CTA
-constexpr int STAGE_FLOATS = R * BOXW;                   // 2176 floats = 8704 B
-constexpr int RING_FLOATS = S * STAGE_FLOATS;
-constexpr size_t SMEM_BYTES = size_t(WARPS) * RING_FLOATS * sizeof(float) + size_t(WARPS) * S * 8;
-constexpr int MIN_ROWS_PER_CTA = 8;                      // quad rows; below this, use fewer CTAs
+constexpr int MIN_TILE_ROWS = 7;            // quad rows per tile (host-side choice)
+constexpr int MAX_TILE_ROWS = 127;
+constexpr int MAX_COUNTERS = 32;            // levels with a work-queue counter pair
 
-static_assert((BOXW * 4) % 16 == 0, "TMA box inner extent must be a multiple of 16 bytes");
-static_assert(BOXW >= SLAB + 5, "smem row must hold 2 halo columns left and 1 right");
+// smem row pitch: TMA writes a box densely (136); the cp.async loader keeps
+// every row's 16-byte alignment shift delta (0..3 floats), hence 4 more.
+template <bool TMA> struct Lay {
+    static constexpr int RP = TMA ? BOXW : BOXW + 4;
+    static constexpr int SUB = (BOXH * RP + 31) / 32 * 32;       // one box; TMA dst is 128-B aligned
+};
+template <bool TMA> struct Ring {
+    static constexpr int STAGE = NBOX * Lay<TMA>::SUB;          // floats per stage
+    static constexpr int FLOATS = S * STAGE;                    // floats per warp ring
+    static constexpr size_t SMEM = size_t(WARPS) * FLOATS * sizeof(float) + size_t(WARPS) * S * 8;
+};
+
+static_assert((Ring<true>::STAGE * 4) % 128 == 0 && (Ring<false>::STAGE * 4) % 128 == 0,
+              "every ring slot must be 128-byte aligned for TMA");
+static_assert(BOXH <= 256, "TMA box extent limit");
+static_assert(QPL == 2 || QPL == 4, "2 or 4 quads per lane");
+
+// smem offsets (floats, from a row of box 0) of what a lane reads
+template <bool TMA>
+__device__ __forceinline__ int lane_offset(int lane)
+{
+    if (QPL == 2) return 4 + 4 * lane;
+    return lane < 16 ? 8 + 8 * lane : Lay<TMA>::SUB + 8 * (lane - 16);
+}
+constexpr int HALO_OFF = (QPL == 2) ? 2 : 6;                    // columns x0-2, x0-1
+template <bool TMA>
+__device__ __forceinline__ constexpr int right_offset() { return (QPL == 2) ? 132 : Lay<TMA>::SUB + 128; }
 
 // ---------------------------------------------------------------------------
-// Kernel arguments (passed as a __grid_constant__ parameter; the TMA
-// descriptor must be 64-byte aligned and live in param/const space)
+// Kernel arguments (a __grid_constant__ parameter: the TMA descriptor must be
+// 64-byte aligned and live in param space)
 // ---------------------------------------------------------------------------
 struct alignas(64) LevelArgs {
-    CUtensorMap tmap;                 // 3-D {W, in_rows, count}, box {BOXW, R, 1}
+    CUtensorMap tmap;                 // 3-D {W, in_rows, count}, box {BOXW, BOXH, 1}
     const float *in;                  // generic loader: image 0, buffer row 0
     const float *in_end;              // one past the last element of the call's input
     long long in_pitch, in_img_stride;
     float *ll, *hl, *lh, *hh;         // subband bases for image 0, output row 0
     long long ll_pitch, ll_img_stride;
     long long out_pitch, out_img_stride;
+    unsigned int *counter;            // [0] tile counter, [1] finished-warp counter (self-resetting)
     int W, H;                         // level input width, (global) height
     int in_row0, in_rows;             // global row of buffer row 0; rows present in the buffer
     int out_q0;                       // global quad row stored at output row 0
-    int ngroups, count;
+    int nslabs, count;
     int qa0, qa1, qb0, qb1;           // quad-row ranges [qa0, qa1) and [qb0, qb1)
-    long long units;                  // count * ngroups * nq
+    int tb;                           // quad rows per tile
+    int nblk_a, nblk;                 // row blocks in range A, in A and B
+    int ntiles;                       // count * nblk * nslabs
+    int nwarps;                       // warps in the grid
 };
 
 // ---------------------------------------------------------------------------
 // PTX helpers (mbarrier, TMA, cp.async, PDL)
 // ---------------------------------------------------------------------------
 __host__ __device__ __forceinline__ int imin(int x, int y) { return x < y ? x : y; }
-__host__ __device__ __forceinline__ long long imin64(long long x, long long y) { return x < y ? x : y; }
+__host__ __device__ __forceinline__ int imax(int x, int y) { return x > y ? x : y; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -129,8 +191,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
         "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
-__device__ __forceinline__ void tma_load_3d(float *dst, const CUtensorMap *map, int x, int y, int z,
-                                            uint64_t *bar)
+__device__ __forceinline__ void tma_load_3d(float *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar)
 {
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
@@ -160,144 +221,301 @@ __device__ __forceinline__ void pdl_launch_dependents()
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+#ifdef DWT2_PROF
+__device__ unsigned long long g_prof[4];   // cycles waiting for stages, cycles working, stages, tiles
+__device__ unsigned long long g_cta[4096][4];   // per CTA: entry, work start, work end (globaltimer ns), smid
+
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
+// Register arithmetic type.  The product is fp64; the
+// fp32 build (-DDWT2_F32MATH) exists only to measure what the arithmetic
+// costs and is never shipped.
+#if defined(DWT2_F32MATH)
+typedef float real;
+#define R_(x) x##f
+#else
+typedef double real;
+#define R_(x) x
+#endif
+
+__device__ __forceinline__ float to_f32(real x) { return (float)x; }   // round to nearest even
+
 // ---------------------------------------------------------------------------
-// One smem row as seen by one lane, widened to fp64.
-//   v0..v3: the lane's 4 pixels (quad columns mq0, mq0+1: a/b or c/d pairs)
-//   l0, l1: the two pixels left of the slab (lane 0's halo quad)
-//   r:      the pixel right of the lane (lane + 1's v0; lane 31 reads smem)
+// Tiles and the work queue.
+//
+// Tile t covers quad rows [qa, qb) (<= tb of them) of one slab of one image.
+// Tiles are ordered image-major, then row block, then slab, so the tiles
+// that warps fetch at about the same time are horizontally adjacent and
+// share their halo columns through L2.  Warps take tiles from a global
+// atomic counter (dynamic load balancing: a B200 runs some SMs' CTAs up to
+// 1.5x slower than others' under full HBM load; static partitions wait for
+// the slowest).  The counter resets itself: the last warp to find the queue
+// empty zeroes it for the next launch, which cannot start its own fetches
+// before this grid completes (stream order / griddepcontrol.wait).
+// ---------------------------------------------------------------------------
+struct Tile {
+    int img, x0, qa, qb;
+};
+
+__device__ __forceinline__ Tile decode_tile(const LevelArgs &a, int t)
+{
+    Tile T;
+    const int per_img = a.nblk * a.nslabs;
+    T.img = t / per_img;
+    const int r = t - T.img * per_img;
+    const int blk = r / a.nslabs;
+    const int slab = r - blk * a.nslabs;
+    T.x0 = slab * SLAB;
+    if (blk < a.nblk_a) {
+        T.qa = a.qa0 + blk * a.tb;
+        T.qb = imin(T.qa + a.tb, a.qa1);
+    } else {
+        T.qa = a.qb0 + (blk - a.nblk_a) * a.tb;
+        T.qb = imin(T.qa + a.tb, a.qb1);
+    }
+    return T;
+}
+
+__device__ __forceinline__ int fetch_tile(const LevelArgs &a, int lane)
+{
+    int t = 0;
+    if (lane == 0) {
+        t = int(atomicAdd(a.counter, 1u));
+        if (t >= a.ntiles) {
+            // queue drained for this warp; the last warp resets both counters
+            if (atomicAdd(a.counter + 1, 1u) == unsigned(a.nwarps - 1)) {
+                atomicExch(a.counter, 0u);
+                atomicExch(a.counter + 1, 0u);
+            }
+        }
+    }
+    t = __shfl_sync(0xffffffffu, t, 0);
+    return t < a.ntiles ? t : -1;
+}
+
+// Row stream of a tile.  r_first = 0 at the image top, else 2 qa - 2.  Stage
+// j holds rows [r_first + ROWS j, r_first + ROWS j + BOXH); pair k = rows
+// (r_first + 2k + 1, r_first + 2k + 2) lies in stage k / PAIRS at offsets
+// (2 (k % PAIRS) + 1, 2 (k % PAIRS) + 2) and yields the predicted values of
+// quad row n_first + k (n_first = 0 at the top, else qa - 1).
+__device__ __forceinline__ int tile_stages(const Tile &T)
+{
+    const int n_first = (T.qa == 0) ? 0 : T.qa - 1;
+    return (T.qb - n_first + PAIRS - 1) / PAIRS;
+}
+
+__device__ __forceinline__ int tile_row0(const Tile &T) { return (T.qa == 0) ? 0 : 2 * T.qa - 2; }
+
+// ---------------------------------------------------------------------------
+// One smem row as seen by one lane, widened to the register type.
+//   v[0 .. 2 QPL): the lane's pixels = QPL quads (a,b / c,d pairs)
+//   r:             the pixel right of the lane (lane + 1's v[0]; lane 31 reads smem)
+//   l0, l1:        the 2 pixels left of the slab (feed lane 0's halo quad)
+//   bp[i], bh:     even rows only: HL' = b - 1/2 (a + a[m+1]) of every quad
+//                  and of the halo quad (the horizontal predict, reused by
+//                  the vertical predict of the quad row above)
 // ---------------------------------------------------------------------------
 struct RowD {
-    double v0, v1, v2, v3, l0, l1, r;
+    real v[2 * QPL];
+    real r, l0, l1;
+    real bp[QPL], bh;
 };
 
 struct EdgeFlags {
-    bool r_from_v2;    // even W, q1 is the last quad: x[W] := x[W-2]
-    bool v2_from_v0;   // even W, q0 is the last quad: x[W] := x[W-2]
-    bool odd_q0_last;  // odd W, q0 is the last quad (only a, c exist)
-    bool odd_q1_last;  // odd W, q1 is the last quad
+    int last;          // index 0..QPL-1 of the image's last quad in this lane, else -1
+    bool evenW;
     bool left_edge;    // lane 0 of the slab at x = 0: H[-1] := H[0]
 };
 
-template <bool TMA>
-__device__ __forceinline__ RowD load_row(const float *p, int lane, const EdgeFlags &ef)
+template <bool TMA, bool EDGE>
+__device__ __forceinline__ RowD load_row(const float *p, int lane, const EdgeFlags &ef, bool even_row)
 {
-    float f0, f1, f2, f3;
+    float f[2 * QPL];
+    const float *q = p + lane_offset<TMA>(lane);
     if (TMA) {
-        const float4 q = *reinterpret_cast<const float4 *>(p + 4 + 4 * lane);
-        f0 = q.x; f1 = q.y; f2 = q.z; f3 = q.w;
+#pragma unroll
+        for (int i = 0; i < QPL / 2; ++i) {
+            const float4 t = *reinterpret_cast<const float4 *>(q + 4 * i);
+            f[4 * i] = t.x; f[4 * i + 1] = t.y; f[4 * i + 2] = t.z; f[4 * i + 3] = t.w;
+        }
     } else {
-        f0 = p[4 + 4 * lane]; f1 = p[5 + 4 * lane]; f2 = p[6 + 4 * lane]; f3 = p[7 + 4 * lane];
+#pragma unroll
+        for (int i = 0; i < 2 * QPL; ++i) f[i] = q[i];
     }
-    const float fl0 = p[2], fl1 = p[3];                 // broadcast reads
-    const float fr31 = p[4 + SLAB];                     // broadcast read
-    const float fr = __shfl_down_sync(0xffffffffu, f0, 1);
+    const float fl0 = p[HALO_OFF], fl1 = p[HALO_OFF + 1];       // broadcast
+    const float fr31 = p[right_offset<TMA>()];                  // broadcast
+    const float fr = __shfl_down_sync(0xffffffffu, f[0], 1);
     RowD d;
-    d.v0 = f0; d.v1 = f1; d.v2 = f2; d.v3 = f3;
-    d.l0 = fl0; d.l1 = fl1;
+#pragma unroll
+    for (int i = 0; i < 2 * QPL; ++i) d.v[i] = f[i];
     d.r = (lane == 31) ? fr31 : fr;
-    if (ef.r_from_v2) d.r = d.v2;
-    if (ef.v2_from_v0) d.v2 = d.v0;
+    d.l0 = fl0;
+    d.l1 = fl1;
+    if (EDGE && ef.evenW) {
+        // even W: the last quad's right neighbour column W is x[W-2] (WSS)
+#pragma unroll
+        for (int i = 0; i < QPL - 1; ++i)
+            if (ef.last == i) d.v[2 * i + 2] = d.v[2 * i];
+        if (ef.last == QPL - 1) d.r = d.v[2 * QPL - 2];
+    }
+    if (even_row) {
+        // horizontal predict HL' = b + P a = b - 1/2 (a + a[m+1])
+#pragma unroll
+        for (int i = 0; i < QPL; ++i) {
+            const real ar = (i < QPL - 1) ? d.v[2 * i + 2] : d.r;
+            d.bp[i] = fma(R_(-0.5), d.v[2 * i] + ar, d.v[2 * i + 1]);
+        }
+        d.bh = fma(R_(-0.5), d.l0 + d.v[0], d.l1);
+    }
     return d;
 }
 
-// Spatial predict of Eq. (5) for one quad (a b / c d) with right (r), lower
-// (dn) and lower-right (rdn) neighbours:
-//   HL' = b + P a            = b - 1/2 (a + a[m+1])
-//   LH' = c + P* a           = c - 1/2 (a + a[n+1])
-//   HH' = d + P* b + P c + PP* a
-//       = d - 1/2 (b + b[n+1]) - 1/2 (c + c[m+1]) + 1/4 (a + a[m+1] + a[n+1] + a[m+1,n+1])
-struct Pred1 {
-    double bp, cp, dp;
-};
-
-__device__ __forceinline__ Pred1 predict_quad(double a, double b, double c, double d, double ar, double cr,
-                                              double adn, double bdn, double ardn)
-{
-    Pred1 p;
-    const double sa = a + ar;
-    p.bp = fma(-0.5, sa, b);
-    p.cp = fma(-0.5, a + adn, c);
-    double t = fma(-0.5, b + bdn, d);
-    t = fma(-0.5, c + cr, t);
-    p.dp = fma(0.25, sa + (adn + ardn), t);
-    return p;
-}
-
-// Predicted values of the lane's two quads of quad row n plus the left
-// neighbour's (m-1) HL' and HH' -- everything the update of row n reads
-// from row n itself.
-struct PredRow {
-    double bp0, cp0, dp0, bp1, cp1, dp1, bl, dl;
-};
-
-__device__ __forceinline__ PredRow predict_row(const RowD &E, const RowD &O, const RowD &N, int lane,
-                                               const EdgeFlags &ef)
-{
-    PredRow p;
-    const Pred1 q0 = predict_quad(E.v0, E.v1, O.v0, O.v1, E.v2, O.v2, N.v0, N.v1, N.v2);
-    const Pred1 q1 = predict_quad(E.v2, E.v3, O.v2, O.v3, E.r, O.r, N.v2, N.v3, N.r);
-    p.bp0 = q0.bp; p.cp0 = q0.cp; p.dp0 = q0.dp;
-    p.bp1 = q1.bp; p.cp1 = q1.cp; p.dp1 = q1.dp;
-    // the single in-level synchronisation of Eq. (5): m-1 neighbours by shuffle
-    double bl = __shfl_up_sync(0xffffffffu, q1.bp, 1);
-    double dl = __shfl_up_sync(0xffffffffu, q1.dp, 1);
-    if (lane == 0) {
-        if (ef.left_edge) {            // H[-1] := H[0]
-            bl = q0.bp;
-            dl = q0.dp;
-        } else {                       // recompute quad m0-1 from the smem halo
-            const Pred1 h = predict_quad(E.l0, E.l1, O.l0, O.l1, E.v0, O.v0, N.l0, N.l1, N.v0);
-            bl = h.bp;
-            dl = h.dp;
-        }
-    }
-    if (ef.odd_q0_last) {              // H[M] := H[M-1] for the last (L-only) column
-        p.bp0 = bl;
-        p.dp0 = dl;
-    }
-    if (ef.odd_q1_last) {
-        p.bp1 = p.bp0;
-        p.dp1 = p.dp0;
-    }
-    p.bl = bl;
-    p.dl = dl;
-    return p;
-}
-
-// Carried state of quad row n-1 (per lane quad): LH', HH' and the horizontal
-// pair sum HH'(m) + HH'(m-1).
+// Spatial predict and spatial update of Eq. (5) for quad row n.
+//
+// Predict (Eq. (5) right factor), per quad with E = row 2n, O = row 2n+1,
+// N = row 2n+2:
+//   HL' = b + P a                        (E.bp, computed with the row)
+//   LH' = c + P* a       = c - 1/2 (a + a[n+1])
+//   HH' = d + P c + P* b + PP* a = d - 1/2 (c + c[m+1]) - 1/2 (HL' + HL'[n+1])
+// (PP* a + P* b = P* (b + P a) = P* HL', so the 4-term PP* stencil is
+// evaluated through HL', which is exact in the fp64 register arithmetic.)
+//
+// Update (Eq. (5) left factor) through the same factorisation:
+//   LH  = LH' + U HH'                     = LH' + 1/4 (HH' + HH'[m-1])
+//   HL  = HL' + U* HH'                    = HL' + 1/4 (HH' + HH'[n-1])
+//   LL  = a + U HL' + U* LH' + UU* HH'    = (a + 1/4 (HL' + HL'[m-1])) + 1/4 (LH + LH[n-1])
+//   HH  = HH'
+// The m-1 neighbours of the lane's first quad come from lane - 1 by
+// shuffle (the single in-level synchronisation `|` of the paper), lane 0
+// computes the halo quad m0-1 itself; the n-1 neighbours are carried in
+// registers from the previous quad row (Carry).
 struct Carry {
-    double cu0, du0, su0, cu1, du1, su1;
+    real lh[QPL], hh[QPL];            // LH and HH' of quad row n-1
+    real hh_halo;                     // HH' of the halo quad m0-1 at n-1 (lane 0)
 };
 
-__device__ __forceinline__ void store2(float *p, float x, float y, bool v0, bool v1, bool vec, bool stream)
+struct Out {
+    float A[QPL], B[QPL], C[QPL], D[QPL];
+};
+
+// Returns the outputs of quad row n; updates the carry to row n.
+// missing_odd: odd H, n is the last quad row (row 2n+1 does not exist):
+// LH', HH' := their values at n-1 (H[M] := H[M-1]).
+template <bool EDGE>
+__device__ __forceinline__ Out predict_update(const RowD &E, const RowD &O, const RowD &N, Carry &cy, int lane,
+                                              const EdgeFlags &ef, bool carry_in, bool missing_odd)
 {
-    if (v1) {
-        if (vec) {
-            if (stream) __stcs(reinterpret_cast<float2 *>(p), make_float2(x, y));
-            else *reinterpret_cast<float2 *>(p) = make_float2(x, y);
-        } else {
-            if (stream) { __stcs(p, x); __stcs(p + 1, y); }
-            else { p[0] = x; p[1] = y; }
+    real cp[QPL], dp[QPL], bp[QPL];
+#pragma unroll
+    for (int i = 0; i < QPL; ++i) {
+        bp[i] = E.bp[i];
+        const real c = O.v[2 * i], d = O.v[2 * i + 1];
+        const real cr = (i < QPL - 1) ? O.v[2 * i + 2] : O.r;
+        cp[i] = fma(R_(-0.5), E.v[2 * i] + N.v[2 * i], c);
+        dp[i] = fma(R_(-0.5), E.bp[i] + N.bp[i], fma(R_(-0.5), c + cr, d));
+    }
+    // halo quad m0 - 1 (columns x0-2, x0-1): every lane computes it (a
+    // masked warp instruction costs the same pipe time); lane 0 keeps it
+    real hdp = fma(R_(-0.5), E.bh + N.bh, fma(R_(-0.5), O.l0 + O.v[0], O.l1));
+    if (missing_odd) {
+#pragma unroll
+        for (int i = 0; i < QPL; ++i) dp[i] = cy.hh[i];
+        hdp = cy.hh_halo;
+    }
+    const real bl_sh = __shfl_up_sync(0xffffffffu, bp[QPL - 1], 1);
+    const real dl_sh = __shfl_up_sync(0xffffffffu, dp[QPL - 1], 1);
+    real bl = (lane == 0) ? E.bh : bl_sh;
+    real dl = (lane == 0) ? hdp : dl_sh;
+    if (EDGE) {
+        if (ef.left_edge) {            // H[-1] := H[0]
+            bl = bp[0];
+            dl = dp[0];
         }
-    } else if (v0) {
-        if (stream) __stcs(p, x);
-        else p[0] = x;
+        if (!ef.evenW) {
+            // odd W: the last column is L-only; H[M] := H[M-1]
+#pragma unroll
+            for (int i = 0; i < QPL; ++i) {
+                if (ef.last == i) {
+                    bp[i] = (i == 0) ? bl : bp[i - 1];
+                    dp[i] = (i == 0) ? dl : dp[i - 1];
+                }
+            }
+        }
+    }
+    Out o;
+    real lh[QPL];
+#pragma unroll
+    for (int i = 0; i < QPL; ++i) {
+        const real dleft = (i == 0) ? dl : dp[i - 1];
+        lh[i] = missing_odd ? cy.lh[i] : fma(R_(0.25), dp[i] + dleft, cp[i]);
+    }
+    cy.hh_halo = hdp;
+    if (carry_in) {
+#pragma unroll
+        for (int i = 0; i < QPL; ++i) {
+            cy.lh[i] = lh[i];
+            cy.hh[i] = dp[i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < QPL; ++i) {
+        const real bleft = (i == 0) ? bl : bp[i - 1];
+        const real a1 = fma(R_(0.25), bp[i] + bleft, E.v[2 * i]);
+        o.A[i] = to_f32(fma(R_(0.25), lh[i] + cy.lh[i], a1));
+        o.B[i] = to_f32(fma(R_(0.25), dp[i] + cy.hh[i], bp[i]));
+        o.C[i] = to_f32(lh[i]);
+        o.D[i] = to_f32(dp[i]);
+        cy.lh[i] = lh[i];
+        cy.hh[i] = dp[i];
+    }
+    return o;
+}
+
+// Stores QPL consecutive coefficients of one subband row; n valid (0..QPL).
+template <bool VEC, bool EDGE>
+__device__ __forceinline__ void storeq(float *p, const float (&x)[QPL], int n, bool stream)
+{
+    if (VEC && (!EDGE || n == QPL)) {
+        if (QPL == 4) {
+            const float4 v = make_float4(x[0], x[1], x[2 % QPL], x[3 % QPL]);
+            if (stream) __stcs(reinterpret_cast<float4 *>(p), v);
+            else *reinterpret_cast<float4 *>(p) = v;
+        } else {
+            const float2 v = make_float2(x[0], x[1]);
+            if (stream) __stcs(reinterpret_cast<float2 *>(p), v);
+            else *reinterpret_cast<float2 *>(p) = v;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < QPL; ++i) {
+            if (!EDGE || i < n) {
+                if (stream) __stcs(p + i, x[i]);
+                else p[i] = x[i];
+            }
+        }
     }
 }
 
 // ---------------------------------------------------------------------------
-// The fused level kernel
+// The fused level kernel: a persistent grid of independent warps; each warp
+// streams tiles from the work queue through its own TMA ring (producer and
+// consumer in one warp, prefetching across tile boundaries).
 // ---------------------------------------------------------------------------
 template <bool TMA, bool VEC>
-__global__ void __launch_bounds__(THREADS)
+__global__ void __launch_bounds__(THREADS, DWT2_MINB)
 dwt53_level_kernel(const __grid_constant__ LevelArgs a)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    float *ring = reinterpret_cast<float *>(smem_raw) + size_t(warp) * RING_FLOATS;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + size_t(WARPS) * RING_FLOATS * sizeof(float)) + warp * S;
+    float *ring = reinterpret_cast<float *>(smem_raw) + size_t(warp) * Ring<TMA>::FLOATS;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + size_t(WARPS) * Ring<TMA>::FLOATS * sizeof(float)) + warp * S;
 
     if (lane == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], TMA ? 1u : 32u);
@@ -312,199 +530,226 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
     // memory, exactly as this grid waits for its predecessor here.
     pdl_launch_dependents();
     pdl_wait();
+#ifdef DWT2_PROF
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_cta[blockIdx.x][0] = gtimer();
+        g_cta[blockIdx.x][3] = smid;
+    }
+    const long long t_work = clock64();
+    long long t_wait = 0;
+#endif
 
-    const int Wq = (a.W + 1) >> 1;          // L columns / LL width
-    const int Wh = a.W >> 1;                // H columns
+    const int Wq = (a.W + 1) >> 1;
+    const int Wh = a.W >> 1;
+    const int Hq = (a.H + 1) >> 1;
     const int Hh = a.H >> 1;
-    const int lenA = a.qa1 - a.qa0;
-    const int nq = lenA + (a.qb1 - a.qb0);
-    const long long per_img = (long long)a.ngroups * nq;
 
-    const long long u_begin = (a.units * blockIdx.x) / gridDim.x;
-    const long long u_end = (a.units * (blockIdx.x + 1)) / gridDim.x;
+    // ---- producer state: the tile whose stages are being issued
+    Tile pt;
+    int pt_id = fetch_tile(a, lane);
+    int pt_j = 0, pt_nst = 0;
+    if (pt_id >= 0) {
+        pt = decode_tile(a, pt_id);
+        pt_nst = tile_stages(pt);
+    }
+    // tile ids handed from producer to consumer, in order (warp-private smem
+    // would do too; S + 1 entries suffice because the producer is at most S
+    // stages -- hence at most S tiles -- ahead)
+    int tq[S + 1];
+#pragma unroll
+    for (int i = 0; i <= S; ++i) tq[i] = -1;
+    int tq_head = 0, tq_tail = 0;      // consumer pops at head, producer pushes at tail
+    if (pt_id >= 0) {
+        tq[0] = pt_id;
+        tq_tail = 1;
+    }
+    uint32_t prod_seq = 0, cons_seq = 0;
 
-    uint32_t stage_ctr = 0;                 // per-warp ring position (monotonic)
+    auto issue_next = [&]() {
+        // issue the next stage of the global stage sequence (if any)
+        if (pt_id < 0) return;
+        if (pt_j == pt_nst) {
+            pt_id = fetch_tile(a, lane);
+            if (pt_id < 0) return;
+            pt = decode_tile(a, pt_id);
+            pt_nst = tile_stages(pt);
+            pt_j = 0;
+#pragma unroll
+            for (int i = 0; i <= S; ++i)
+                if (i == tq_tail % (S + 1)) tq[i] = pt_id;
+            ++tq_tail;
+        }
+        const int slot = int(prod_seq % S);
+        float *dst = ring + slot * Ring<TMA>::STAGE;
+        const int r0 = tile_row0(pt) + pt_j * ROWS;
+        if (TMA) {
+            if (lane == 0) {
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&bars[slot], uint32_t(NBOX * BOXH * BOXW * sizeof(float)));
+                tma_load_3d(dst, &a.tmap, pt.x0 + BOX0, r0 - a.in_row0, pt.img, &bars[slot]);
+                if (NBOX == 2)
+                    tma_load_3d(dst + Lay<TMA>::SUB, &a.tmap, pt.x0 + BOX1, r0 - a.in_row0, pt.img, &bars[slot]);
+            }
+        } else {
+            // per box and row: 35 aligned 16-byte chunks cover [start - delta, start + 140 - delta)
+            const float *img_in = a.in + (long long)pt.img * a.in_img_stride;
+            constexpr int CPR = Lay<false>::RP / 4;
+            for (int idx = lane; idx < NBOX * BOXH * CPR; idx += 32) {
+                const int bx = idx / (BOXH * CPR);
+                const int rem = idx - bx * (BOXH * CPR);
+                const int rr = rem / CPR;
+                const int c = rem - rr * CPR;
+                const int br = r0 + rr - a.in_row0;
+                uint32_t nbytes = 0;     // 0: zero-fill, no global access
+                const char *src = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(a.in) & ~uintptr_t(15));
+                if (br >= 0 && br < a.in_rows) {
+                    const float *rowp = img_in + (long long)br * a.in_pitch + (pt.x0 + (bx ? BOX1 : BOX0));
+                    const uintptr_t al = reinterpret_cast<uintptr_t>(rowp) & ~uintptr_t(15);
+                    const uintptr_t ch = al + uintptr_t(16) * c;
+                    const uintptr_t lo = reinterpret_cast<uintptr_t>(a.in);
+                    const uintptr_t hi = reinterpret_cast<uintptr_t>(a.in_end);
+                    if (ch < hi && ch + 16 > lo) {
+                        nbytes = uint32_t((hi - ch) < 16 ? (hi - ch) : 16);
+                        src = reinterpret_cast<const char *>(ch);
+                    }
+                }
+                cp_async_16(dst + bx * Lay<false>::SUB + rr * Lay<false>::RP + 4 * c, src, nbytes);
+            }
+            cp_async_mbar_arrive(&bars[slot]);
+        }
+        ++pt_j;
+        ++prod_seq;
+    };
 
-    for (long long u = u_begin; u < u_end;) {
-        // ---- decode the segment: maximal run of units with equal (img, group, range)
-        const int img = int(u / per_img);
-        const long long rem = u - (long long)img * per_img;
-        const int group = int(rem / nq);
-        const int qi = int(rem - (long long)group * nq);
-        const bool inA = qi < lenA;
-        const int run_left = inA ? lenA - qi : nq - qi;
-        const int seg_len = int(imin64(run_left, u_end - u));
-        const int qa = inA ? a.qa0 + qi : a.qb0 + (qi - lenA);
-        const int qb = qa + seg_len;
-        u += seg_len;
+    // prologue: fill the ring
+    for (int i = 0; i < S; ++i) issue_next();
 
-        const int x0 = (group * WARPS + warp) * SLAB;
-        if (x0 >= a.W) continue;            // warp-uniform: no pixels in this slab
+    // ---- consumer: tiles in the order the producer fetched them
+    while (tq_head < tq_tail) {
+        int t_id = -1;
+#pragma unroll
+        for (int i = 0; i <= S; ++i)
+            if (i == tq_head % (S + 1)) t_id = tq[i];
+        ++tq_head;
+        const Tile T = decode_tile(a, t_id);
+        const int x0 = T.x0;
+        const int img = T.img;
+        const bool edge = (x0 == 0) || ((x0 >> 1) + SLAB / 2 >= Wq - 1);
 
-        // ---- per-lane constants
-        const int mq0 = (x0 >> 1) + 2 * lane;
+        const int mq0 = (x0 >> 1) + QPL * lane;
         EdgeFlags ef;
-        const bool evenW = (a.W & 1) == 0;
-        ef.r_from_v2 = evenW && (mq0 + 1 == Wq - 1);
-        ef.v2_from_v0 = evenW && (mq0 == Wq - 1);
-        ef.odd_q0_last = !evenW && (mq0 == Wq - 1);
-        ef.odd_q1_last = !evenW && (mq0 + 1 == Wq - 1);
+        ef.evenW = (a.W & 1) == 0;
+        ef.last = (Wq - 1 - mq0 >= 0 && Wq - 1 - mq0 < QPL) ? Wq - 1 - mq0 : -1;
         ef.left_edge = (x0 == 0) && (lane == 0);
-        const bool L0 = mq0 < Wq, L1 = mq0 + 1 < Wq;
-        const bool H0 = mq0 < Wh, H1 = mq0 + 1 < Wh;
+        const int nL = imax(0, imin(QPL, Wq - mq0));
+        const int nH = imax(0, imin(QPL, Wh - mq0));
 
-        // ---- row stream: global rows [r_first, r_last]
-        const bool top = (qa == 0);
-        const int r_first = top ? 0 : 2 * qa - 2;
-        const int r_last = imin(2 * qb, a.H - 1);
-        const int nst = (r_last - r_first + R) / R;
-        const uint32_t base = stage_ctr;
-        stage_ctr += nst;
-
+        const bool top = (T.qa == 0);
+        const int r_first = tile_row0(T);
+        const int n_first = top ? 0 : T.qa - 1;
+        const int npairs = T.qb - n_first;
+        const bool bottom = (T.qb == Hq);
+        const int nst = tile_stages(T);
         const float *img_in = a.in + (long long)img * a.in_img_stride;
 
-        auto issue = [&](int j) {
-            const uint32_t k = base + j;
-            const int slot = int(k % S);
-            float *dst = ring + slot * STAGE_FLOATS;
-            const int r0 = r_first + j * R;
-            if (TMA) {
-                if (lane == 0) {
-                    fence_proxy_async();
-                    mbar_arrive_expect_tx(&bars[slot], uint32_t(STAGE_FLOATS * sizeof(float)));
-                    tma_load_3d(dst, &a.tmap, x0 - 4, r0 - a.in_row0, img, &bars[slot]);
-                }
-            } else {
-                // 34 aligned 16-byte chunks per row cover [x0-4-delta, x0+132-delta)
-                for (int idx = lane; idx < R * (BOXW / 4); idx += 32) {
-                    const int rr = idx / (BOXW / 4);
-                    const int c = idx - rr * (BOXW / 4);
-                    const int br = r0 + rr - a.in_row0;
-                    uint32_t nbytes = 0;     // 0: zero-fill, no global access
-                    const char *src = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(a.in) & ~uintptr_t(15));
-                    if (br >= 0 && br < a.in_rows) {
-                        const float *rowp = img_in + (long long)br * a.in_pitch + (x0 - 4);
-                        const uintptr_t al = reinterpret_cast<uintptr_t>(rowp) & ~uintptr_t(15);
-                        const uintptr_t ch = al + uintptr_t(16) * c;
-                        const uintptr_t lo = reinterpret_cast<uintptr_t>(a.in);
-                        const uintptr_t hi = reinterpret_cast<uintptr_t>(a.in_end);
-                        if (ch < hi && ch + 16 > lo) {
-                            nbytes = uint32_t((hi - ch) < 16 ? (hi - ch) : 16);
-                            src = reinterpret_cast<const char *>(ch);
-                        }
-                    }
-                    cp_async_16(dst + rr * BOXW + 4 * c, src, nbytes);
-                }
-                cp_async_mbar_arrive(&bars[slot]);
-            }
-        };
+        // output cursors (all subbands advance one row per quad row)
+        const int orow = T.qa - a.out_q0;
+        float *pll = a.ll + (long long)img * a.ll_img_stride + (long long)orow * a.ll_pitch + mq0;
+        const long long ob = (long long)img * a.out_img_stride + (long long)orow * a.out_pitch + mq0;
+        float *phl = a.hl + ob, *plh = a.lh + ob, *phh = a.hh + ob;
 
-        __syncwarp();                        // previous segment's reads of the ring are done
-        for (int j = 0; j < imin(nst, S); ++j) issue(j);
-
-        int waited = -1, released = 0;
-        auto row_ptr = [&](int r) -> const float * {
-            const int j = (r - r_first) / R;
-            if (j > waited) {
-                const uint32_t k = base + j;
-                mbar_wait(&bars[k % S], (k / S) & 1u);
-                waited = j;
-            }
-            const float *p = ring + int((base + j) % S) * STAGE_FLOATS + ((r - r_first) - j * R) * BOXW;
-            if (!TMA) {
-                const int br = r - a.in_row0;
-                if (br >= 0 && br < a.in_rows) {
-                    const float *rowp = img_in + (long long)br * a.in_pitch + (x0 - 4);
-                    p += int((reinterpret_cast<uintptr_t>(rowp) >> 2) & 3);
-                }
-            }
-            return p;
-        };
-        auto release_through = [&](int r) {  // every stage whose rows are all <= r is consumed
-            const int done = (r - r_first + 1) / R;
-            while (released < done) {
-                if (released + S < nst) {
-                    __syncwarp();
-                    issue(released + S);
-                }
-                ++released;
-            }
-        };
-
-        RowD E = load_row<TMA>(row_ptr(r_first), lane, ef);
-        RowD O, N;
         Carry cy;
-        int n0 = qa;
-        if (!top) {
-            // carry-in: predicted values of quad row qa-1 (rows 2qa-2 .. 2qa)
-            O = load_row<TMA>(row_ptr(2 * qa - 1), lane, ef);
-            N = load_row<TMA>(row_ptr(2 * qa), lane, ef);
-            release_through(2 * qa);
-            const PredRow p = predict_row(E, O, N, lane, ef);
-            cy.cu0 = p.cp0; cy.du0 = p.dp0; cy.su0 = p.dp0 + p.dl;
-            cy.cu1 = p.cp1; cy.du1 = p.dp1; cy.su1 = p.dp1 + p.dp0;
-            E = N;
+        RowD E;
+        for (int j = 0; j < nst; ++j) {
+            const uint32_t k = cons_seq++;
+            const float *slot = ring + int(k % S) * Ring<TMA>::STAGE;
+#ifdef DWT2_PROF
+            const long long tw = clock64();
+#endif
+            mbar_wait(&bars[k % S], (k / S) & 1u);
+#ifdef DWT2_PROF
+            t_wait += clock64() - tw;
+#endif
+            auto rowp = [&](int off) -> const float * {
+                const float *p = slot + off * Lay<TMA>::RP;
+                if (!TMA) {
+                    const int br = r_first + j * ROWS + off - a.in_row0;
+                    if (br >= 0 && br < a.in_rows) {
+                        const float *g = img_in + (long long)br * a.in_pitch + (x0 + BOX0);
+                        p += int((reinterpret_cast<uintptr_t>(g) >> 2) & 3);
+                    }
+                }
+                return p;
+            };
+            auto body = [&](auto edge_tag) {
+                constexpr bool EG = decltype(edge_tag)::value;
+                if (j == 0) E = load_row<TMA, EG>(rowp(0), lane, ef, true);
+                const int k0 = j * PAIRS;
+                const int kend = imin(k0 + PAIRS, npairs);
+                const bool has_special_end = bottom && (kend == npairs);
+                if (j > 0 && kend - k0 == PAIRS && !has_special_end) {
+                    // steady state: PAIRS regular pairs, fully unrolled
+#pragma unroll
+                    for (int i = 0; i < PAIRS; ++i) {
+                        const RowD O = load_row<TMA, EG>(rowp(2 * i + 1), lane, ef, false);
+                        const RowD N = load_row<TMA, EG>(rowp(2 * i + 2), lane, ef, true);
+                        const Out o = predict_update<EG>(E, O, N, cy, lane, ef, false, false);
+                        storeq<VEC, EG>(pll, o.A, nL, false);
+                        storeq<VEC, EG>(phl, o.B, nH, true);
+                        storeq<VEC, EG>(plh, o.C, nL, true);
+                        storeq<VEC, EG>(phh, o.D, nH, true);
+                        pll += a.ll_pitch; phl += a.out_pitch; plh += a.out_pitch; phh += a.out_pitch;
+                        E = N;
+                    }
+                } else {
+                    for (int kk = k0; kk < kend; ++kk) {
+                        const int i = kk - k0;
+                        const int n = n_first + kk;
+                        const bool last = bottom && (kk == npairs - 1);
+                        const bool has_odd = !last || (2 * n + 1 <= a.H - 1);
+                        const bool has_next = !last || (2 * n + 2 <= a.H - 1);
+                        RowD O, N;
+                        if (has_odd) {
+                            O = load_row<TMA, EG>(rowp(2 * i + 1), lane, ef, false);
+                            N = has_next ? load_row<TMA, EG>(rowp(2 * i + 2), lane, ef, true)
+                                         : E;        // even H: x[H] := x[H-2]
+                        } else {
+                            O = E;                   // odd H: row 2n+1 is missing
+                            N = E;
+                        }
+                        // carry-in pair: quad row qa-1 (or row -1 mirroring row 0 at the top)
+                        const bool cin = (kk == 0);
+                        const Out o = predict_update<EG>(E, O, N, cy, lane, ef, cin, !has_odd);
+                        if (!(cin && !top)) {
+                            storeq<VEC, true>(pll, o.A, nL, false);
+                            storeq<VEC, true>(phl, o.B, nH, true);
+                            if (n < Hh) {
+                                storeq<VEC, true>(plh, o.C, nL, true);
+                                storeq<VEC, true>(phh, o.D, nH, true);
+                            }
+                            pll += a.ll_pitch; phl += a.out_pitch; plh += a.out_pitch; phh += a.out_pitch;
+                        }
+                        E = N;
+                    }
+                }
+            };
+            if (edge) body(std::integral_constant<bool, true>());
+            else body(std::integral_constant<bool, false>());
+            // stage consumed: its slot takes the next stage of the sequence
+            __syncwarp();
+            issue_next();
         }
-
-        const long long oimg = (long long)img * a.out_img_stride;
-        const long long limg = (long long)img * a.ll_img_stride;
-
-        for (int n = n0; n < qb; ++n) {
-            const bool has_odd = (2 * n + 1) <= a.H - 1;
-            const bool has_next = (2 * n + 2) <= a.H - 1;
-            PredRow p;
-            double s0, s1;                   // HH'(m) + HH'(m-1) per lane quad
-            if (has_odd) {
-                O = load_row<TMA>(row_ptr(2 * n + 1), lane, ef);
-                if (has_next) N = load_row<TMA>(row_ptr(2 * n + 2), lane, ef);
-                else N = E;                  // even H: x[H] := x[H-2]
-                release_through(has_next ? 2 * n + 2 : 2 * n + 1);
-                p = predict_row(E, O, N, lane, ef);
-                s0 = p.dp0 + p.dl;
-                s1 = p.dp1 + p.dp0;
-            } else {
-                // odd H, last quad row: only row 2n exists.  HL' needs no
-                // vertical neighbour; LH', HH' (and their m-1 sums) := their
-                // values at n-1 (H[M] := H[M-1]).
-                release_through(2 * n);
-                p = predict_row(E, E, E, lane, ef);
-                p.cp0 = cy.cu0; p.dp0 = cy.du0;
-                p.cp1 = cy.cu1; p.dp1 = cy.du1;
-                s0 = cy.su0;
-                s1 = cy.su1;
-            }
-            if (n == 0) {                    // top edge: row -1 mirrors row 0
-                cy.cu0 = p.cp0; cy.du0 = p.dp0; cy.su0 = s0;
-                cy.cu1 = p.cp1; cy.du1 = p.dp1; cy.su1 = s1;
-            }
-            // spatial update (Eq. (5) left factor)
-            //   LL = a + U HL' + U* LH' + UU* HH'
-            //   HL = HL' + U* HH';  LH = LH' + U HH';  HH = HH'
-            const double A0 = E.v0 + 0.25 * (p.bp0 + p.bl) + 0.25 * (p.cp0 + cy.cu0) + 0.0625 * (s0 + cy.su0);
-            const double A1 = E.v2 + 0.25 * (p.bp1 + p.bp0) + 0.25 * (p.cp1 + cy.cu1) + 0.0625 * (s1 + cy.su1);
-            const double B0 = fma(0.25, p.dp0 + cy.du0, p.bp0);
-            const double B1 = fma(0.25, p.dp1 + cy.du1, p.bp1);
-            const double C0 = fma(0.25, s0, p.cp0);
-            const double C1 = fma(0.25, s1, p.cp1);
-
-            const int orow = n - a.out_q0;
-            float *pll = a.ll + limg + (long long)orow * a.ll_pitch + mq0;
-            float *phl = a.hl + oimg + (long long)orow * a.out_pitch + mq0;
-            store2(pll, __double2float_rn(A0), __double2float_rn(A1), L0, L1, VEC, false);
-            store2(phl, __double2float_rn(B0), __double2float_rn(B1), H0, H1, VEC, true);
-            if (n < Hh) {
-                float *plh = a.lh + oimg + (long long)orow * a.out_pitch + mq0;
-                float *phh = a.hh + oimg + (long long)orow * a.out_pitch + mq0;
-                store2(plh, __double2float_rn(C0), __double2float_rn(C1), L0, L1, VEC, true);
-                store2(phh, __double2float_rn(p.dp0), __double2float_rn(p.dp1), H0, H1, VEC, true);
-            }
-
-            cy.cu0 = p.cp0; cy.du0 = p.dp0; cy.su0 = s0;
-            cy.cu1 = p.cp1; cy.du1 = p.dp1; cy.su1 = s1;
-            E = N;
-        }
-        release_through(r_last);             // (all stages are waited for by now)
     }
+#ifdef DWT2_PROF
+    if (lane == 0) {
+        atomicAdd(&g_prof[0], (unsigned long long)t_wait);
+        atomicAdd(&g_prof[1], (unsigned long long)(clock64() - t_work));
+        atomicAdd(&g_prof[2], (unsigned long long)cons_seq);
+    }
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_cta[blockIdx.x][2] = gtimer();
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -562,7 +807,8 @@ struct dwt2_plan {
     float *scratch[2];
     long long sc_pitch[2], sc_img_stride[2];
     size_t scratch_bytes;
-    int max_ctas;
+    int max_ctas[2];          // resident CTAs: [0] cp.async kernels, [1] TMA kernels
+    unsigned int *counters;   // per level: tile queue + finished-warp counter (device, self-resetting)
     // host e2e staging
     mutable float *d_in, *d_out;
     mutable cudaStream_t s_h2d, s_d2h;
@@ -584,8 +830,8 @@ struct LaunchIO {
     int count;
 };
 
-int32_t launch_level(const dwt2_plan *p, int W, int H, const LaunchIO &io, int qa0, int qa1, int qb0, int qb1,
-                     cudaStream_t stream)
+int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO &io, int qa0, int qa1, int qb0,
+                     int qb1, cudaStream_t stream)
 {
     LevelArgs a;
     memset(&a, 0, sizeof(a));
@@ -607,40 +853,58 @@ int32_t launch_level(const dwt2_plan *p, int W, int H, const LaunchIO &io, int q
     a.in_row0 = io.in_row0;
     a.in_rows = io.in_rows;
     a.out_q0 = io.out_q0;
-    a.ngroups = (W + GROUP - 1) / GROUP;
+    a.nslabs = (W + SLAB - 1) / SLAB;
     a.count = io.count;
     a.qa0 = qa0; a.qa1 = qa1; a.qb0 = qb0; a.qb1 = qb1;
-    const int nq = (qa1 - qa0) + (qb1 - qb0);
-    a.units = (long long)io.count * a.ngroups * nq;
-    if (a.units == 0) return DWT2_OK;
+    const int lenA = qa1 - qa0, lenB = qb1 - qb0;
+    const long long slab_rows = (long long)io.count * a.nslabs * (lenA + lenB);
+    if (slab_rows == 0) return DWT2_OK;
 
     const bool tma = aligned(io.in, 16) && (io.in_pitch * 4) % 16 == 0 &&
                      (io.count == 1 || (io.in_img_stride * 4) % 16 == 0);
-    const bool vec = aligned(a.ll, 8) && aligned(a.hl, 8) && aligned(a.lh, 8) && aligned(a.hh, 8) &&
-                     io.ll_pitch % 2 == 0 && io.out_pitch % 2 == 0 &&
-                     (io.count == 1 || (io.ll_img_stride % 2 == 0 && io.out_img_stride % 2 == 0));
+    const int va = (QPL == 4) ? 16 : 8;        // subband store width in bytes
+    const bool vec = aligned(a.ll, va) && aligned(a.hl, va) && aligned(a.lh, va) && aligned(a.hh, va) &&
+                     io.ll_pitch % QPL == 0 && io.out_pitch % QPL == 0 &&
+                     (io.count == 1 || (io.ll_img_stride % QPL == 0 && io.out_img_stride % QPL == 0));
     if (tma) {
         PFN_cuTensorMapEncodeTiled_v12000 enc = get_encode();
         if (!enc) return fail(DWT2_ECUDA);
         cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)io.in_rows, (cuuint64_t)io.count};
         long long img_bytes = io.count > 1 ? io.in_img_stride * 4 : round_up(io.in_pitch * 4 * io.in_rows, 16);
         cuuint64_t strides[2] = {(cuuint64_t)(io.in_pitch * 4), (cuuint64_t)img_bytes};
-        cuuint32_t box[3] = {(cuuint32_t)BOXW, (cuuint32_t)R, 1};
+        cuuint32_t box[3] = {(cuuint32_t)BOXW, (cuuint32_t)BOXH, 1};
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = enc(&a.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(io.in), dims, strides,
                          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         DWT2_L2_PROMOTION, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(DWT2_ECUDA);
     }
 
-    const long long max_units_ctas = (a.units + MIN_ROWS_PER_CTA - 1) / MIN_ROWS_PER_CTA;
-    const int grid = int(std::max<long long>(1, std::min<long long>(p->max_ctas, max_units_ctas)));
+    // Persistent grid of independent warps pulling tiles of tb quad rows x
+    // one slab.  tb: about 8 tiles per warp for load balance, between 8 and
+    // 127 quad rows (tb + 1 pairs incl. the carry-in fill whole stages).
+    const int max_ctas = p->max_ctas[tma ? 1 : 0];
+    const long long warps_full = (long long)max_ctas * WARPS;
+    long long tb = slab_rows / (8 * warps_full);
+    tb = std::max<long long>(MIN_TILE_ROWS, std::min<long long>(MAX_TILE_ROWS, tb));
+    tb = std::max<long long>(MIN_TILE_ROWS, (tb + 1) / PAIRS * PAIRS - 1);
+    a.tb = int(tb);
+    a.nblk_a = (lenA + a.tb - 1) / a.tb;
+    a.nblk = a.nblk_a + (lenB + a.tb - 1) / a.tb;
+    const long long ntiles = (long long)io.count * a.nblk * a.nslabs;
+    if (ntiles >= (1LL << 31)) return fail(DWT2_EINVAL);
+    a.ntiles = int(ntiles);
+    const long long want_ctas = (ntiles + WARPS - 1) / WARPS;
+    const int grid = int(std::max<long long>(1, std::min<long long>(max_ctas, want_ctas)));
+    a.nwarps = grid * WARPS;
+    if (level < 0 || level >= MAX_COUNTERS) return fail(DWT2_EINVAL);
+    a.counter = p->counters + 2 * level;
 
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.dynamicSmemBytes = tma ? Ring<true>::SMEM : Ring<false>::SMEM;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -657,7 +921,7 @@ int32_t launch_level(const dwt2_plan *p, int W, int H, const LaunchIO &io, int q
 
 int32_t configure_kernels(int *max_ctas)
 {
-    static int cached = 0;
+    static int cached[2] = {0, 0};
     static std::once_flag once;
     static int32_t status = DWT2_OK;
     std::call_once(once, [] {
@@ -669,22 +933,26 @@ int32_t configure_kernels(int *max_ctas)
             status = DWT2_ECUDA;
             return;
         }
-        for (KernelFn f : fns) {
-            if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES)) !=
-                cudaSuccess) {
+        for (int i = 0; i < 4; ++i) {
+            const size_t smem = i < 2 ? Ring<true>::SMEM : Ring<false>::SMEM;
+            if (cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
                 status = DWT2_ECUDA;
                 return;
             }
         }
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[0], THREADS, SMEM_BYTES) != cudaSuccess ||
-            per_sm < 1) {
-            status = DWT2_ECUDA;
-            return;
+        for (int t = 0; t < 2; ++t) {   // t = 1: TMA kernels
+            const size_t smem = t ? Ring<true>::SMEM : Ring<false>::SMEM;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[t ? 0 : 2], THREADS, smem) != cudaSuccess ||
+                per_sm < 1) {
+                status = DWT2_ECUDA;
+                return;
+            }
+            cached[t] = sms * per_sm;
         }
-        cached = sms * per_sm;
     });
     cudaGetLastError();
-    *max_ctas = cached;
+    max_ctas[0] = cached[0];
+    max_ctas[1] = cached[1];
     return status;
 }
 
@@ -737,12 +1005,23 @@ dwt2_plan *make_plan(int W, int H, int levels, int boundary, int max_count, bool
         w = (w + 1) / 2;
         h = (h + 1) / 2;
     }
-    int32_t st = configure_kernels(&p->max_ctas);
+    int32_t st = configure_kernels(p->max_ctas);
     if (st != DWT2_OK) {
         delete p;
         g_last_error = st;
         return nullptr;
     }
+    // work-queue counters (zeroed once; every launch leaves them zeroed)
+    const size_t cbytes = sizeof(unsigned int) * 2 * MAX_COUNTERS;
+    if (cudaMalloc(&p->counters, cbytes) != cudaSuccess || cudaMemset(p->counters, 0, cbytes) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
+        cudaGetLastError();
+        if (p->counters) cudaFree(p->counters);
+        delete p;
+        g_last_error = DWT2_ENOMEM;
+        return nullptr;
+    }
+    p->scratch_bytes += cbytes;
     // LL scratch: level k (1-based, k < levels) writes LL_k to scratch[(k-1) % 2]
     for (int s = 0; s < 2; ++s) {
         if (levels >= s + 2) {
@@ -753,6 +1032,7 @@ dwt2_plan *make_plan(int W, int H, int levels, int boundary, int max_count, bool
             if (cudaMalloc(&p->scratch[s], bytes) != cudaSuccess) {
                 cudaGetLastError();
                 if (p->scratch[0]) cudaFree(p->scratch[0]);
+                cudaFree(p->counters);
                 delete p;
                 g_last_error = DWT2_ENOMEM;
                 return nullptr;
@@ -825,7 +1105,7 @@ int32_t run_levels(const dwt2_plan *p, const float *in, float *out, int count, l
             qa = q1a;
             qb = q1b;
         }
-        int32_t r = launch_level(p, g.W, g.H, io, qa, qb, 0, 0, s);
+        int32_t r = launch_level(p, k, g.W, g.H, io, qa, qb, 0, 0, s);
         if (r != DWT2_OK) return r;
     }
     return DWT2_OK;
@@ -837,6 +1117,33 @@ int32_t run_levels(const dwt2_plan *p, const float *in, float *out, int count, l
 // C ABI
 // ---------------------------------------------------------------------------
 extern "C" {
+
+// Measurement builds only (-DDWT2_PROF): per-CTA timestamps; not in dwt2.h.
+int32_t dwt2_debug_cta(unsigned long long *out, int32_t n)
+{
+#ifdef DWT2_PROF
+    return cudaMemcpyFromSymbol(out, g_cta, sizeof(unsigned long long) * 4 * n) == cudaSuccess ? DWT2_OK : DWT2_ECUDA;
+#else
+    (void)out; (void)n;
+    return DWT2_EUNSUPPORTED;
+#endif
+}
+
+// Measurement builds only (-DDWT2_PROF): per-warp cycle counters; not in dwt2.h.
+int32_t dwt2_debug_prof(unsigned long long *out4, int32_t reset)
+{
+#ifdef DWT2_PROF
+    if (cudaMemcpyFromSymbol(out4, g_prof, sizeof(unsigned long long) * 4) != cudaSuccess) return DWT2_ECUDA;
+    if (reset) {
+        unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+    }
+    return DWT2_OK;
+#else
+    (void)out4; (void)reset;
+    return DWT2_EUNSUPPORTED;
+#endif
+}
 
 dwt2_plan *dwt2_plan_create(int32_t width, int32_t height, int32_t levels, int32_t boundary)
 {
@@ -933,7 +1240,7 @@ int32_t dwt2_forward_strip(const dwt2_plan *p, const float *in, float *out, int3
         b0 = std::max(ib, ia); b1 = qe;
         if (b0 < a1) b0 = a1;
     }
-    int32_t r = launch_level(p, p->W, p->Hg, io, a0, a1, b0, b1, reinterpret_cast<cudaStream_t>(stream));
+    int32_t r = launch_level(p, 0, p->W, p->Hg, io, a0, a1, b0, b1, reinterpret_cast<cudaStream_t>(stream));
     if (r != DWT2_OK) return r;
     g_last_error = DWT2_OK;
     return DWT2_OK;
@@ -1023,6 +1330,7 @@ int32_t dwt2_forward_host(const dwt2_plan *p, const float *host_in, float *host_
 void dwt2_destroy(dwt2_plan *p)
 {
     if (!p) return;
+    if (p->counters) cudaFree(p->counters);
     for (int s = 0; s < 2; ++s)
         if (p->scratch[s]) cudaFree(p->scratch[s]);
     if (p->d_in) {

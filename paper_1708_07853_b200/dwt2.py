@@ -13,7 +13,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libdwt2.so")
+LIB_PATH = os.environ.get("DWT2_LIB") or os.path.join(_PKG, "libdwt2.so")   # DWT2_LIB: tuning variants
 
 DWT2_OK, DWT2_EINVAL, DWT2_ENOMEM, DWT2_ECUDA, DWT2_EUNSUPPORTED = 0, -1, -2, -3, -4
 DWT2_BOUNDARY_SYMMETRIC = 0
