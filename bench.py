@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--config", default="3", choices=["1", "2", "3", "4", "4b", "5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-overlap", action="store_true", help="strips: exchange, then one launch")
+    ap.add_argument("--no-graph", action="store_true", help="launch every step from the host instead of "
+                    "replaying a CUDA graph of it")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=0, help="oracle sample rows (0 = auto)")
@@ -218,33 +220,35 @@ class OursRunner:
             self.D.strip_forward_step(self.ex, self.splan, self.out, overlap=not self.overlap_off)
 
     def level1_kernel_ms(self, iters):
-        """Average duration of the dominant kernel (level 1), CUDA events on its stream."""
+        """Average duration of the dominant kernel (level 1: 3/4 of the
+        algorithmic bytes of a pyramid), CUDA events on its launch stream,
+        through level-1-only plans on the same buffers."""
         torch = self.torch
         s = torch.cuda.current_stream()
         if self.mode == "single" and self.cfg.levels == 1:
             return None   # identical to the step: caller uses the step time
         if self.mode == "strip":
             return None
-        # time level-1-only plans on the same buffers
+        if self.mode == "single":
+            plans = [(self.dwt2.Plan(self.cfg.groups[0].width, self.cfg.groups[0].height, 1), self.x, self.out)]
+        else:
+            plans = [(self.dwt2.Plan(p.width, p.height, 1, max_count=x.shape[0]), x, o) for p, x, o in self.items]
+        for p, x, o in plans:          # warm-up (tensor maps, first-launch costs)
+            p.forward(x, o)
+        torch.cuda.synchronize()
         ts = []
         for _ in range(iters):
             if self.flush is not None:
                 self.flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
-            if self.mode == "single":
-                self._l1plan = getattr(self, "_l1plan", None) or self.dwt2.Plan(self.cfg.groups[0].width,
-                                                                                self.cfg.groups[0].height, 1)
-                self._l1plan.forward(self.x, self.out)
-            else:
-                if not hasattr(self, "_l1items"):
-                    self._l1items = [(self.dwt2.Plan(p.width, p.height, 1, max_count=x.shape[0]), x, o)
-                                     for p, x, o in self.items]
-                for p, x, o in self._l1items:
-                    p.forward(x, o)
+            for p, x, o in plans:
+                p.forward(x, o)
             e1.record(s)
             e1.synchronize()
             ts.append(e0.elapsed_time(e1))
+        for p, _, _ in plans:
+            p.close()
         return sum(ts) / len(ts)
 
     def e2e(self, steps, warm):
@@ -402,6 +406,17 @@ def main():
     for _ in range(max(3, args.warmup)):
         runner.step()
     torch.cuda.synchronize()
+    graph = None
+    if not args.no_graph and runner.mode != "strip":
+        # one step as a CUDA graph (the level kernels keep their programmatic
+        # dependent-launch edges); replaying it removes host launch gaps
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            runner.step()
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize()
+    do_step = graph.replay if graph is not None else runner.step
 
     sampler = ClockSampler(local)
     sampler.start()
@@ -412,7 +427,7 @@ def main():
     t_host0 = time.perf_counter()
     e0.record(stream)
     for _ in range(args.steps):
-        runner.step()
+        do_step()
     e1.record(stream)
     torch.cuda.synchronize()
     t_host1 = time.perf_counter()
@@ -483,6 +498,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": runner.launches * args.steps,
+            "launch": "CUDA graph replay of one step" if graph is not None else "host launches",
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

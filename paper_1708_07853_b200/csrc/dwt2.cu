@@ -64,16 +64,19 @@ namespace {
 #define DWT2_QPL 2
 #endif
 #ifndef DWT2_PAIRS
-#define DWT2_PAIRS 8
+#define DWT2_PAIRS 4
 #endif
 #ifndef DWT2_STAGES
-#define DWT2_STAGES 3
+#define DWT2_STAGES 2
 #endif
 #ifndef DWT2_WARPS
 #define DWT2_WARPS 4
 #endif
 #ifndef DWT2_MINB
-#define DWT2_MINB 1
+#define DWT2_MINB 4
+#endif
+#ifndef DWT2_TPW
+#define DWT2_TPW 32                 // target tiles per warp on large levels (measured optimum)
 #endif
 #ifndef DWT2_L2_PROMOTION
 #define DWT2_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_NONE
@@ -146,6 +149,7 @@ struct alignas(64) LevelArgs {
     int nblk_a, nblk;                 // row blocks in range A, in A and B
     int ntiles;                       // count * nblk * nslabs
     int nwarps;                       // warps in the grid
+    int static_tiles;                 // 1: tile w -> warp w, no work queue
 };
 
 // ---------------------------------------------------------------------------
@@ -282,8 +286,13 @@ __device__ __forceinline__ Tile decode_tile(const LevelArgs &a, int t)
     return T;
 }
 
-__device__ __forceinline__ int fetch_tile(const LevelArgs &a, int lane)
+__device__ __forceinline__ int fetch_tile(const LevelArgs &a, int lane, bool &first)
 {
+    if (a.static_tiles) {
+        const int t = first ? int(blockIdx.x * WARPS + (threadIdx.x >> 5)) : a.ntiles;
+        first = false;
+        return t < a.ntiles ? t : -1;
+    }
     int t = 0;
     if (lane == 0) {
         t = int(atomicAdd(a.counter, 1u));
@@ -548,7 +557,8 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
 
     // ---- producer state: the tile whose stages are being issued
     Tile pt;
-    int pt_id = fetch_tile(a, lane);
+    bool first_fetch = true;
+    int pt_id = fetch_tile(a, lane, first_fetch);
     int pt_j = 0, pt_nst = 0;
     if (pt_id >= 0) {
         pt = decode_tile(a, pt_id);
@@ -571,7 +581,7 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
         // issue the next stage of the global stage sequence (if any)
         if (pt_id < 0) return;
         if (pt_j == pt_nst) {
-            pt_id = fetch_tile(a, lane);
+            pt_id = fetch_tile(a, lane, first_fetch);
             if (pt_id < 0) return;
             pt = decode_tile(a, pt_id);
             pt_nst = tile_stages(pt);
@@ -809,6 +819,16 @@ struct dwt2_plan {
     size_t scratch_bytes;
     int max_ctas[2];          // resident CTAs: [0] cp.async kernels, [1] TMA kernels
     unsigned int *counters;   // per level: tile queue + finished-warp counter (device, self-resetting)
+    // host-side caches (the API serialises calls on one plan)
+    struct TmapCache {
+        const float *in;
+        long long pitch, stride;
+        int W, rows, count;
+        CUtensorMap map;
+    };
+    mutable TmapCache tcache[MAX_COUNTERS];
+    mutable const void *valid_ptr[4];       // device pointers already checked by on_plan_device
+    mutable int valid_next;
     // host e2e staging
     mutable float *d_in, *d_out;
     mutable cudaStream_t s_h2d, s_d2h;
@@ -866,7 +886,12 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     const bool vec = aligned(a.ll, va) && aligned(a.hl, va) && aligned(a.lh, va) && aligned(a.hh, va) &&
                      io.ll_pitch % QPL == 0 && io.out_pitch % QPL == 0 &&
                      (io.count == 1 || (io.ll_img_stride % QPL == 0 && io.out_img_stride % QPL == 0));
-    if (tma) {
+    if (level < 0 || level >= MAX_COUNTERS) return fail(DWT2_EINVAL);
+    dwt2_plan::TmapCache &tc = p->tcache[level];
+    if (tma && tc.in == io.in && tc.pitch == io.in_pitch && tc.stride == io.in_img_stride && tc.W == W &&
+        tc.rows == io.in_rows && tc.count == io.count) {
+        a.tmap = tc.map;                      // same input tensor as the last launch of this level
+    } else if (tma) {
         PFN_cuTensorMapEncodeTiled_v12000 enc = get_encode();
         if (!enc) return fail(DWT2_ECUDA);
         cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)io.in_rows, (cuuint64_t)io.count};
@@ -878,16 +903,22 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
                          box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                          DWT2_L2_PROMOTION, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(DWT2_ECUDA);
+        tc.in = io.in; tc.pitch = io.in_pitch; tc.stride = io.in_img_stride;
+        tc.W = W; tc.rows = io.in_rows; tc.count = io.count;
+        tc.map = a.tmap;
     }
 
-    // Persistent grid of independent warps pulling tiles of tb quad rows x
-    // one slab.  tb: about 8 tiles per warp for load balance, between 8 and
-    // 127 quad rows (tb + 1 pairs incl. the carry-in fill whole stages).
+    // Grid of independent warps, each streaming tiles of tb quad rows x one
+    // slab.  Large levels: a persistent grid pulls ~4 tiles per warp from the
+    // work queue (load balance).  Small levels (at most one tile per resident
+    // warp): tile w goes to warp w, no queue.  tb + 1 pairs (incl. the
+    // carry-in pair) fill whole stages.
     const int max_ctas = p->max_ctas[tma ? 1 : 0];
     const long long warps_full = (long long)max_ctas * WARPS;
-    long long tb = slab_rows / (8 * warps_full);
-    tb = std::max<long long>(MIN_TILE_ROWS, std::min<long long>(MAX_TILE_ROWS, tb));
-    tb = std::max<long long>(MIN_TILE_ROWS, (tb + 1) / PAIRS * PAIRS - 1);
+    long long tb = slab_rows / (DWT2_TPW * warps_full);
+    if (tb < MIN_TILE_ROWS) tb = (slab_rows + warps_full - 1) / warps_full;
+    tb = std::max<long long>(PAIRS - 1, std::min<long long>(MAX_TILE_ROWS, tb));
+    tb = std::max<long long>(PAIRS - 1, (tb + 1 + PAIRS - 1) / PAIRS * PAIRS - 1);
     a.tb = int(tb);
     a.nblk_a = (lenA + a.tb - 1) / a.tb;
     a.nblk = a.nblk_a + (lenB + a.tb - 1) / a.tb;
@@ -897,7 +928,7 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     const long long want_ctas = (ntiles + WARPS - 1) / WARPS;
     const int grid = int(std::max<long long>(1, std::min<long long>(max_ctas, want_ctas)));
     a.nwarps = grid * WARPS;
-    if (level < 0 || level >= MAX_COUNTERS) return fail(DWT2_EINVAL);
+    a.static_tiles = ntiles <= a.nwarps ? 1 : 0;
     a.counter = p->counters + 2 * level;
 
     cudaLaunchConfig_t cfg;
@@ -1052,12 +1083,19 @@ bool overlap(const void *a, size_t an, const void *b, size_t bn)
 
 bool on_plan_device(const dwt2_plan *p, const void *ptr)
 {
+    for (int i = 0; i < 4; ++i)
+        if (p->valid_ptr[i] == ptr) return true;
     cudaPointerAttributes at;
     if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
-    return (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) && at.device == p->device;
+    const bool ok = (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) && at.device == p->device;
+    if (ok) {
+        p->valid_ptr[p->valid_next] = ptr;
+        p->valid_next = (p->valid_next + 1) & 3;
+    }
+    return ok;
 }
 
 // Forward of levels [first, last] for `count` images.  Level 1 reads `in`.
