@@ -1,0 +1,115 @@
+"""Multi-process host logic of the multi-GPU paths, on CPU with the gloo backend.
+
+* Row strips (config 3): after StripExchange's grouped send/recv, every
+  rank's input buffer must equal the global image rows
+  [r_g - ghost_top, r_{g+1} + ghost_bot) -- exactly what the level kernel
+  reads (2 ghost rows above, 1 below; Eq. (5) supports).  Strip
+  outputs placed by place_strip_output must tile the global Mallat layout.
+* Batches (config 5): shards cover every image exactly once.
+
+world sizes 2 and 3 (an interior rank has both neighbours).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1708_07853_b200 import distributed as D
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, W, H, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        img = (np.arange(H * W, dtype=np.float32).reshape(H, W) % 251.0).astype(np.float32)
+        ex = D.StripExchange(W, H, rank, world, device="cpu")
+        ex.buf.fill_(-1.0)
+        ex.strip.copy_(torch.from_numpy(img[ex.r0:ex.r1]))
+        reqs = ex.start()
+        ex.finish(reqs)
+        lo, hi = ex.r0 - ex.ghost_top, ex.r1 + ex.ghost_bot
+        ok = np.array_equal(ex.buf.numpy(), img[lo:hi])
+        q.put((rank, ok, ex.r0, ex.r1, ex.ghost_top, ex.ghost_bot))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,W,H", [(2, 40, 30), (3, 33, 17), (3, 64, 64)])
+def test_strip_halo_exchange_gloo(world, W, H):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, W, H, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    for rank, ok, r0, r1, gt, gb in res:
+        assert ok, f"rank {rank}: ghost rows wrong"
+        assert gt == (2 if r0 > 0 else 0) and gb == (1 if r1 < H else 0)
+    # strips tile the image
+    assert res[0][2] == 0 and res[-1][3] == H
+    for a, b in zip(res, res[1:]):
+        assert a[3] == b[2] and a[2] % 2 == 0
+
+
+def test_strip_partition_rules():
+    for H in [2, 3, 17, 64, 101, 16384]:
+        for G in [1, 2, 3, 4, 8]:
+            if H < 2 * G:
+                continue
+            prev = 0
+            for g in range(G):
+                r0, r1 = D.strip_rows(H, g, G)
+                assert r0 == prev and r0 % 2 == 0 and r1 > r0
+                assert (r1 % 2 == 0) or r1 == H
+                prev = r1
+            assert prev == H
+            sizes = [D.strip_rows(H, g, G)[1] - D.strip_rows(H, g, G)[0] for g in range(G)]
+            assert max(sizes) - min(sizes) <= 3
+
+
+def test_halo_plan_messages_match():
+    """Every send has a matching receive on the peer with the same row count."""
+    H, G = 100, 4
+    plans = {g: D.halo_plan(H, g, G) for g in range(G)}
+    for g, msgs in plans.items():
+        for op, peer, _, n in msgs:
+            if op == "send":
+                assert ("recv", g, n) in [(o, p, m) for o, p, _, m in plans[peer]]
+
+
+def test_place_and_take_strip_output_roundtrip():
+    rng = np.random.default_rng(0)
+    for W, H, G in [(10, 14, 3), (9, 17, 4), (16, 16, 2)]:
+        full = rng.standard_normal((H, W)).astype(np.float32)
+        rebuilt = np.full_like(full, np.nan)
+        for g in range(G):
+            r0, r1 = D.strip_rows(H, g, G)
+            D.place_strip_output(rebuilt, D.take_strip_output(full, W, H, r0, r1), W, H, r0, r1)
+        np.testing.assert_array_equal(rebuilt, full)
+
+
+def test_batch_shards_cover():
+    for count in [1, 5, 32, 256]:
+        for G in [1, 2, 3, 8]:
+            seen = []
+            for g in range(G):
+                seen.extend(D.shard(count, g, G))
+            assert seen == list(range(count))
