@@ -129,6 +129,51 @@ int32_t dwt2_forward_strip(const dwt2_plan *plan, const float *in, float *out, i
 int32_t dwt2_forward_host(const dwt2_plan *plan, const float *host_in, float *host_out,
                           dwt2_stream_t stream);
 
+/* Inverse transform of one image: the Mallat pyramid
+ * `in` (W x H fp32, pitch W, as dwt2_forward writes it) is reconstructed
+ * into the W x H image `out`, coarsest level first.  Each level undoes the
+ * spatial update, then the spatial predict of Eq. (5) (
+ * steps reversed and negated) in one fused kernel, with the
+ * same whole-sample symmetric extension as the forward.  fp64 in registers,
+ * every level's reconstruction stored as fp32 (intermediate levels in the
+ * plan's scratch).  Same ownership, overlap and stream rules as
+ * dwt2_forward; strip plans are rejected (DWT2_EINVAL).  For integer-valued
+ * inputs in [0, 255] and <= 2 levels, dwt2_inverse(dwt2_forward(x)) == x bit
+ * for bit. */
+int32_t dwt2_inverse(const dwt2_plan *plan, const float *in, float *out, dwt2_stream_t stream);
+
+/* Batched inverse: `count` pyramids, element strides as in
+ * dwt2_forward_batched.  One launch per level covers all images. */
+int32_t dwt2_inverse_batched(const dwt2_plan *plan, const float *in, float *out, int32_t count,
+                             int64_t in_stride, int64_t out_stride, dwt2_stream_t stream);
+
+/* Schemes of the paper, for the comparison of SURVEY.md 8f row N1 (PAPER.md
+ * section 4, Fig. 6): the same transform computed with one kernel per
+ * barrier-separated step of each scheme (a step boundary that exchanges
+ * data across the image is a kernel boundary, i.e. an HBM round trip). */
+enum {
+    DWT2_SCHEME_FUSED = 0,          /* Eq. (5) fused into one kernel per level (the product path) */
+    DWT2_SCHEME_NONSEP_NAIVE = 1,   /* Eq. (5), one plain kernel, predicted neighbours recomputed */
+    DWT2_SCHEME_NONSEP_LIFTING = 2, /* Eq. (5): spatial predict | spatial update (2 kernels) */
+    DWT2_SCHEME_NONSEP_ADAPTED = 3, /* Fig. 3: Eq. (5) with the constants P0, U0 split off (2 kernels) */
+    DWT2_SCHEME_SEP_CONV = 4,       /* Eq. (4): horizontal | vertical filter bank (2 kernels) */
+    DWT2_SCHEME_SEP_LIFTING = 5     /* Eq. (3): 4 separable lifting steps (4 kernels) */
+};
+
+/* Kernel launches (barrier-separated steps) per level of a scheme, or
+ * DWT2_EINVAL for an unknown scheme. */
+int32_t dwt2_scheme_steps(int32_t scheme);
+
+/* Forward transform of `count` images (strides as in dwt2_forward_batched)
+ * with the given scheme.  Same result as dwt2_forward up to fp32 rounding of
+ * the intermediates between steps (bit-exact for integer-valued inputs at
+ * <= 2 levels).  The 2-step schemes (except NONSEP_NAIVE and SEP_LIFTING,
+ * which work in place on `out`) use a plan-owned work buffer of count x W x H
+ * fp32, allocated on first use (so the first call is not capture-safe).
+ * DWT2_SCHEME_FUSED is dwt2_forward_batched. */
+int32_t dwt2_forward_scheme(const dwt2_plan *plan, int32_t scheme, const float *in, float *out, int32_t count,
+                            int64_t in_stride, int64_t out_stride, dwt2_stream_t stream);
+
 /* Frees the plan and its device memory (cudaFree synchronises the device).
  * NULL is a no-op.  No work using the plan may be in flight. */
 void dwt2_destroy(dwt2_plan *plan);

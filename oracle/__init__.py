@@ -52,7 +52,7 @@ def _load():
         lib.oracle_dwt53_fwd_lifting.restype = L
         lib.oracle_dwt53_fwd_conv.argtypes = [dp, dp, L, L, L, ctypes.c_int]
         lib.oracle_dwt53_fwd_conv.restype = L
-        lib.oracle_dwt53_inv_lifting.argtypes = [dp, dp, L, L, L]
+        lib.oracle_dwt53_inv_lifting.argtypes = [dp, dp, L, L, L, ctypes.c_int]
         lib.oracle_dwt53_inv_lifting.restype = L
         lib.oracle_dwt53_conv_sample_f32.argtypes = [fp, L, L, L, L, ip, lp, lp, dp]
         lib.oracle_dwt53_conv_sample.argtypes = [dp, L, L, L, L, ip, lp, lp, dp]
@@ -98,11 +98,13 @@ def forward(img, levels: int = 1, round_f32: bool = False, algorithm: str = "lif
     return out
 
 
-def inverse(coeffs, levels: int = 1) -> np.ndarray:
+def inverse(coeffs, levels: int = 1, round_f32: bool = False) -> np.ndarray:
+    """Multi-level inverse (algorithm C) of a Mallat pyramid, fp64.
+    round_f32: round every level's reconstruction to fp32 (the GPU storage type)."""
     c = np.ascontiguousarray(coeffs, dtype=np.float64)
     H, W = c.shape
     out = np.empty_like(c)
-    if _load().oracle_dwt53_inv_lifting(_dptr(c), _dptr(out), W, H, levels) < 0:
+    if _load().oracle_dwt53_inv_lifting(_dptr(c), _dptr(out), W, H, levels, int(bool(round_f32))) < 0:
         raise ValueError("oracle: invalid arguments")
     return out
 

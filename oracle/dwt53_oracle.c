@@ -300,8 +300,12 @@ long oracle_dwt53_fwd_conv(const double *in, double *out, long W, long H, long l
     return multilevel(in, out, W, H, levels, round_f32, 1);
 }
 
-/* Algorithm C: inverse of A (levels in reverse order, each level inverted). */
-long oracle_dwt53_inv_lifting(const double *in, double *out, long W, long H, long levels)
+/* Algorithm C: inverse of A (levels in reverse order, each level inverted).
+ * round_f32: round each level's reconstruction to fp32 before the next
+ * (finer) level reads it -- the storage type of the GPU path (DESIGN.md
+ * reading C-A13); 0 keeps everything fp64. */
+long oracle_dwt53_inv_lifting(const double *in, double *out, long W, long H, long levels,
+                              int round_f32)
 {
     long k, *ws, *hs;
     if (W < 1 || H < 1 || levels < 0)
@@ -315,8 +319,11 @@ long oracle_dwt53_inv_lifting(const double *in, double *out, long W, long H, lon
         hs[k] = (hs[k - 1] + 1) / 2;
     }
     memcpy(out, in, (size_t)W * (size_t)H * sizeof(double));
-    for (k = levels - 1; k >= 0; k--)
+    for (k = levels - 1; k >= 0; k--) {
         level_inv_lifting(out, W, out, W, ws[k], hs[k]);
+        if (round_f32)
+            round_region_f32(out, W, ws[k], hs[k]);
+    }
     free(ws);
     free(hs);
     return levels;

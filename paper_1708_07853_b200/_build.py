@@ -1,7 +1,7 @@
 """Compile the CUDA library in-tree for sm_100a (used by __graft_entry__.build()).
 
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared -Xcompiler -fPIC
-  csrc/dwt2.cu -> paper_1708_07853_b200/libdwt2.so   (links only cudart; the TMA
+  csrc/{dwt2,inverse,schemes}.cu -> paper_1708_07853_b200/libdwt2.so   (links only cudart; the TMA
 descriptor encoder is fetched from the driver at run time).
 """
 from __future__ import annotations
@@ -11,7 +11,8 @@ import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-SRC = os.path.join(PKG, "csrc", "dwt2.cu")
+SRCS = [os.path.join(PKG, "csrc", f) for f in ("dwt2.cu", "inverse.cu", "schemes.cu")]
+DEPS = SRCS + [os.path.join(PKG, "csrc", "dwt2_internal.h")]
 HDR = os.path.join(ROOT, "include", "dwt2.h")
 LIB = os.path.join(PKG, "libdwt2.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -28,7 +29,7 @@ def build_variant(name: str, defines: dict) -> str:
     out_dir = os.path.join(ROOT, "build", "variants")
     os.makedirs(out_dir, exist_ok=True)
     out = os.path.join(out_dir, f"libdwt2_{name}.so")
-    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{k}={v}" for k, v in defines.items()], SRC, "-o", out]
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{k}={v}" for k, v in defines.items()], *SRCS, "-o", out]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
@@ -37,10 +38,10 @@ def build_variant(name: str, defines: dict) -> str:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     stale = (not os.path.exists(LIB) or
-             os.path.getmtime(LIB) < max(os.path.getmtime(SRC), os.path.getmtime(HDR)))
+             os.path.getmtime(LIB) < max([os.path.getmtime(f) for f in DEPS] + [os.path.getmtime(HDR)]))
     if force or stale:
         tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [NVCC, *NVCC_FLAGS, SRC, "-o", tmp]
+        cmd = [NVCC, *NVCC_FLAGS, *SRCS, "-o", tmp]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

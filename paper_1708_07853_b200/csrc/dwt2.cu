@@ -40,12 +40,15 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
 #include <type_traits>
 
-#include "../../include/dwt2.h"
+#include "dwt2_internal.h"
+
+using namespace dwt2_detail;
 
 namespace {
 
@@ -75,6 +78,9 @@ namespace {
 #ifndef DWT2_MINB
 #define DWT2_MINB 4
 #endif
+#ifndef DWT2_MIN_TPW
+#define DWT2_MIN_TPW 2
+#endif
 #ifndef DWT2_TPW
 #define DWT2_TPW 32                 // target tiles per warp on large levels (measured optimum)
 #endif
@@ -95,9 +101,9 @@ constexpr int BOXH = ROWS + 1;              // a stage holds rows [r, r + ROWS +
 constexpr int S = DWT2_STAGES;              // stages per warp ring
 constexpr int WARPS = DWT2_WARPS;           // warps per CTA (independent; packing only)
 constexpr int THREADS = WARPS * 32;
-constexpr int MIN_TILE_ROWS = 7;            // quad rows per tile (host-side choice)
+constexpr int MIN_TILE_ROWS = 11;           // min quad rows per tile (sweep: 11 > 7, 15 on 4096^2 and 8192^2)
 constexpr int MAX_TILE_ROWS = 127;
-constexpr int MAX_COUNTERS = 32;            // levels with a work-queue counter pair
+constexpr int MAX_COUNTERS = MAX_LEVELS;    // levels with a work-queue counter pair
 
 // smem row pitch: TMA writes a box densely (136); the cp.async loader keeps
 // every row's 16-byte alignment shift delta (0..3 floats), hence 4 more.
@@ -765,14 +771,6 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
-thread_local int32_t g_last_error = DWT2_OK;
-
-int32_t fail(int32_t code)
-{
-    g_last_error = code;
-    return code;
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 get_encode()
 {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -787,11 +785,6 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode()
     return fn;
 }
 
-struct LevelGeom {
-    int W, H;            // level input size
-    int Wq, Hq;          // LL size
-};
-
 typedef void (*KernelFn)(LevelArgs);
 
 KernelFn kernel_for(bool tma, bool vec)
@@ -800,40 +793,8 @@ KernelFn kernel_for(bool tma, bool vec)
     return vec ? dwt53_level_kernel<false, true> : dwt53_level_kernel<false, false>;
 }
 
-bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
-
-long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
-
 }  // namespace
 
-struct dwt2_plan {
-    int W, H, levels, max_count;
-    int device;
-    // strip plans
-    bool strip;
-    int Hg, row_begin, row_end, ghost_top, ghost_bot;
-    // geometry and scratch
-    LevelGeom geom[32];
-    float *scratch[2];
-    long long sc_pitch[2], sc_img_stride[2];
-    size_t scratch_bytes;
-    int max_ctas[2];          // resident CTAs: [0] cp.async kernels, [1] TMA kernels
-    unsigned int *counters;   // per level: tile queue + finished-warp counter (device, self-resetting)
-    // host-side caches (the API serialises calls on one plan)
-    struct TmapCache {
-        const float *in;
-        long long pitch, stride;
-        int W, rows, count;
-        CUtensorMap map;
-    };
-    mutable TmapCache tcache[MAX_COUNTERS];
-    mutable const void *valid_ptr[4];       // device pointers already checked by on_plan_device
-    mutable int valid_next;
-    // host e2e staging
-    mutable float *d_in, *d_out;
-    mutable cudaStream_t s_h2d, s_d2h;
-    mutable cudaEvent_t ev[64];
-};
 
 namespace {
 
@@ -849,6 +810,31 @@ struct LaunchIO {
     int out_q0, hq_local;     // strip-local quad row 0, LL rows present in out (LH offset)
     int count;
 };
+
+// Tile-size policy of the work queue (measured on B200).
+// DWT2_TPW / DWT2_MIN_TB / DWT2_MIN_TPW in the environment override it for
+// tuning sweeps (read once per process).
+struct TilePolicy {
+    int tpw;       // target tiles per warp on large levels
+    int min_tb;    // minimum quad rows per tile
+    int min_tpw;   // below this many tiles per warp: one tile per warp, no queue
+};
+
+const TilePolicy &tile_policy()
+{
+    static TilePolicy pol;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        auto env = [](const char *name, int dflt) {
+            const char *v = getenv(name);
+            return (v && atoi(v) > 0) ? atoi(v) : dflt;
+        };
+        pol.tpw = env("DWT2_TPW", DWT2_TPW);
+        pol.min_tb = env("DWT2_MIN_TB", MIN_TILE_ROWS);
+        pol.min_tpw = env("DWT2_MIN_TPW", DWT2_MIN_TPW);
+    });
+    return pol;
+}
 
 int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO &io, int qa0, int qa1, int qb0,
                      int qb1, cudaStream_t stream)
@@ -915,8 +901,15 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     // carry-in pair) fill whole stages.
     const int max_ctas = p->max_ctas[tma ? 1 : 0];
     const long long warps_full = (long long)max_ctas * WARPS;
-    long long tb = slab_rows / (DWT2_TPW * warps_full);
-    if (tb < MIN_TILE_ROWS) tb = (slab_rows + warps_full - 1) / warps_full;
+    const TilePolicy &pol = tile_policy();
+    long long tb = slab_rows / ((long long)pol.tpw * warps_full);
+    if (tb < pol.min_tb) {
+        // fewer than tpw tiles per warp even at the minimum tile height: keep
+        // the minimum height (queue balancing) while that still gives every
+        // warp at least min_tpw tiles, else one tile per warp (small levels)
+        tb = pol.min_tb;
+        if (slab_rows / (tb * warps_full) < pol.min_tpw) tb = (slab_rows + warps_full - 1) / warps_full;
+    }
     tb = std::max<long long>(PAIRS - 1, std::min<long long>(MAX_TILE_ROWS, tb));
     tb = std::max<long long>(PAIRS - 1, (tb + 1 + PAIRS - 1) / PAIRS * PAIRS - 1);
     a.tb = int(tb);
@@ -1019,6 +1012,7 @@ dwt2_plan *make_plan(int W, int H, int levels, int boundary, int max_count, bool
     p->levels = levels;
     p->max_count = max_count;
     p->device = dev;
+    p->sms = prop.multiProcessorCount;
     p->strip = strip;
     p->Hg = Hg;
     p->row_begin = rb;
@@ -1075,11 +1069,11 @@ dwt2_plan *make_plan(int W, int H, int levels, int boundary, int max_count, bool
     return p;
 }
 
-bool overlap(const void *a, size_t an, const void *b, size_t bn)
-{
-    const char *x = static_cast<const char *>(a), *y = static_cast<const char *>(b);
-    return x < y + bn && y < x + an;
-}
+}  // namespace
+
+namespace dwt2_detail {
+
+thread_local int32_t g_last_error = DWT2_OK;
 
 bool on_plan_device(const dwt2_plan *p, const void *ptr)
 {
@@ -1097,6 +1091,10 @@ bool on_plan_device(const dwt2_plan *p, const void *ptr)
     }
     return ok;
 }
+
+}  // namespace dwt2_detail
+
+namespace {
 
 // Forward of levels [first, last] for `count` images.  Level 1 reads `in`.
 // Level-1 quad rows may be restricted to [q1a, q1b) (host pipelining).
@@ -1371,6 +1369,7 @@ void dwt2_destroy(dwt2_plan *p)
     if (p->counters) cudaFree(p->counters);
     for (int s = 0; s < 2; ++s)
         if (p->scratch[s]) cudaFree(p->scratch[s]);
+    if (p->work) cudaFree(p->work);
     if (p->d_in) {
         cudaFree(p->d_in);
         cudaFree(p->d_out);

@@ -1,0 +1,84 @@
+// dwt2_internal.h -- state shared by the translation units behind the C ABI
+// of include/dwt2.h (forward level kernel: dwt2.cu; inverse: inverse.cu;
+// kernel-per-step scheme variants: schemes.cu).  Not installed, not part of
+// the ABI.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/dwt2.h"
+
+namespace dwt2_detail {
+
+constexpr int MAX_LEVELS = 32;
+
+struct LevelGeom {
+    int W, H;            // level input size
+    int Wq, Hq;          // LL size: ceil(W / 2) x ceil(H / 2)
+};
+
+extern thread_local int32_t g_last_error;
+
+inline int32_t fail(int32_t code)
+{
+    g_last_error = code;
+    return code;
+}
+
+inline bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+inline long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
+
+inline bool overlap(const void *a, size_t an, const void *b, size_t bn)
+{
+    const char *x = static_cast<const char *>(a), *y = static_cast<const char *>(b);
+    return x < y + bn && y < x + an;
+}
+
+}  // namespace dwt2_detail
+
+struct dwt2_plan {
+    int W, H, levels, max_count;
+    int device;
+    // strip plans
+    bool strip;
+    int Hg, row_begin, row_end, ghost_top, ghost_bot;
+    // geometry and scratch: level k (0-based) has input geom[k]; the LL of
+    // level k < levels-1 lives in scratch[k % 2] (pitch sc_pitch, per-image
+    // stride sc_img_stride).  The inverse reuses the same buffers: the
+    // reconstructed input of level k >= 1 goes to scratch[(k - 1) % 2].
+    dwt2_detail::LevelGeom geom[dwt2_detail::MAX_LEVELS];
+    float *scratch[2];
+    long long sc_pitch[2], sc_img_stride[2];
+    size_t scratch_bytes;
+    int max_ctas[2];          // resident CTAs of the forward kernel: [0] cp.async, [1] TMA
+    int sms;                  // multiprocessors of the plan's device
+    unsigned int *counters;   // per level: tile queue + finished-warp counter (device, self-resetting)
+    // host-side caches (the API serialises calls on one plan)
+    struct TmapCache {
+        const float *in;
+        long long pitch, stride;
+        int W, rows, count;
+        CUtensorMap map;
+    };
+    mutable TmapCache tcache[dwt2_detail::MAX_LEVELS];
+    mutable const void *valid_ptr[4];       // device pointers already checked by on_plan_device
+    mutable int valid_next;
+    // scheme variants (schemes.cu): one full-size work buffer, allocated lazily
+    mutable float *work;
+    mutable size_t work_bytes;
+    // host e2e staging
+    mutable float *d_in, *d_out;
+    mutable cudaStream_t s_h2d, s_d2h;
+    mutable cudaEvent_t ev[64];
+};
+
+namespace dwt2_detail {
+
+// true if ptr is device (or managed) memory of the plan's device (cached)
+bool on_plan_device(const dwt2_plan *p, const void *ptr);
+
+}  // namespace dwt2_detail

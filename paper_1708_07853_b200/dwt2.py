@@ -18,6 +18,8 @@ LIB_PATH = os.environ.get("DWT2_LIB") or os.path.join(_PKG, "libdwt2.so")   # DW
 DWT2_OK, DWT2_EINVAL, DWT2_ENOMEM, DWT2_ECUDA, DWT2_EUNSUPPORTED = 0, -1, -2, -3, -4
 DWT2_BOUNDARY_SYMMETRIC = 0
 DWT2_STRIP_ALL, DWT2_STRIP_INTERIOR, DWT2_STRIP_BOUNDARY = 0, 1, 2
+SCHEMES = {"fused": 0, "nonsep_naive": 1, "nonsep_lifting": 2, "nonsep_adapted": 3, "sep_conv": 4,
+           "sep_lifting": 5}
 
 # symbol -> (restype, argtypes); mirrors include/dwt2.h exactly
 _P = ctypes.c_void_p
@@ -39,6 +41,10 @@ SIGNATURES = {
     "dwt2_forward_batched": (_I32, [_P, _P, _P, _I32, _I64, _I64, _P]),
     "dwt2_forward_strip": (_I32, [_P, _P, _P, _I32, _P]),
     "dwt2_forward_host": (_I32, [_P, _P, _P, _P]),
+    "dwt2_inverse": (_I32, [_P, _P, _P, _P]),
+    "dwt2_inverse_batched": (_I32, [_P, _P, _P, _I32, _I64, _I64, _P]),
+    "dwt2_scheme_steps": (_I32, [_I32]),
+    "dwt2_forward_scheme": (_I32, [_P, _I32, _P, _P, _I32, _I64, _I64, _P]),
     "dwt2_destroy": (None, [_P]),
     "dwt2_plan_info": (_I32, [_P, ctypes.POINTER(PlanInfo)]),
     "dwt2_last_error": (_I32, []),
@@ -123,6 +129,27 @@ def dwt2_forward_host(plan, host_in_ptr, host_out_ptr, stream):
     _check(lib().dwt2_forward_host(plan, host_in_ptr, host_out_ptr, stream), "dwt2_forward_host")
 
 
+def dwt2_inverse(plan, in_ptr, out_ptr, stream):
+    _check(lib().dwt2_inverse(plan, in_ptr, out_ptr, stream), "dwt2_inverse")
+
+
+def dwt2_inverse_batched(plan, in_ptr, out_ptr, count, in_stride, out_stride, stream):
+    _check(lib().dwt2_inverse_batched(plan, in_ptr, out_ptr, count, in_stride, out_stride, stream),
+           "dwt2_inverse_batched")
+
+
+def dwt2_scheme_steps(scheme):
+    r = lib().dwt2_scheme_steps(scheme)
+    if r < 0:
+        raise DWT2Error(r, "dwt2_scheme_steps")
+    return r
+
+
+def dwt2_forward_scheme(plan, scheme, in_ptr, out_ptr, count, in_stride, out_stride, stream):
+    _check(lib().dwt2_forward_scheme(plan, scheme, in_ptr, out_ptr, count, in_stride, out_stride, stream),
+           "dwt2_forward_scheme")
+
+
 def dwt2_destroy(plan):
     lib().dwt2_destroy(plan)
 
@@ -180,6 +207,39 @@ class Plan:
             dwt2_forward_batched(self._p, x.data_ptr(), out.data_ptr(), n, img, img, _stream_handle(stream))
         return out
 
+    def forward_scheme(self, scheme, x, out=None, stream=None):
+        """Forward transform with one of the paper's schemes (SCHEMES), one
+        kernel per step; scheme "fused" is forward()."""
+        _check_image(x, "x")
+        if tuple(x.shape[-2:]) != (self.height, self.width):
+            raise ValueError(f"expected (..., {self.height}, {self.width}), got {tuple(x.shape)}")
+        import torch
+        if out is None:
+            out = torch.empty_like(x)
+        _check_image(out, "out")
+        img = self.width * self.height
+        n = x.numel() // img
+        code = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
+        dwt2_forward_scheme(self._p, code, x.data_ptr(), out.data_ptr(), n, img, img, _stream_handle(stream))
+        return out
+
+    def inverse(self, y, out=None, stream=None):
+        """Reconstruct (H, W) or (N, H, W) images from their Mallat pyramids."""
+        _check_image(y, "y")
+        if tuple(y.shape[-2:]) != (self.height, self.width):
+            raise ValueError(f"expected (..., {self.height}, {self.width}), got {tuple(y.shape)}")
+        import torch
+        if out is None:
+            out = torch.empty_like(y)
+        _check_image(out, "out")
+        if y.dim() == 2:
+            dwt2_inverse(self._p, y.data_ptr(), out.data_ptr(), _stream_handle(stream))
+        else:
+            n = y.numel() // (self.width * self.height)
+            img = self.width * self.height
+            dwt2_inverse_batched(self._p, y.data_ptr(), out.data_ptr(), n, img, img, _stream_handle(stream))
+        return out
+
     def forward_host(self, host_in, host_out, stream=None):
         """host_in / host_out: CPU float32 tensors (pinned for full speed)."""
         dwt2_forward_host(self._p, host_in.data_ptr(), host_out.data_ptr(), _stream_handle(stream))
@@ -227,6 +287,17 @@ class StripPlan:
             self.close()
         except Exception:
             pass
+
+
+def inverse(y, levels: int = 1):
+    """One-shot inverse DWT of a (H, W) or (N, H, W) CUDA float32 Mallat pyramid."""
+    p = Plan(y.shape[-1], y.shape[-2], levels, max_count=max(1, y.numel() // (y.shape[-1] * y.shape[-2])))
+    try:
+        return p.inverse(y)
+    finally:
+        import torch
+        torch.cuda.current_stream().synchronize()
+        p.close()
 
 
 def forward(x, levels: int = 1):
