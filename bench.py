@@ -135,8 +135,8 @@ def describe(cfg, world):
     return {"workload": f"config {cfg.name}: {cfg.description}", "images": images, "levels": cfg.levels,
             "pixels": cfg.pixels, "input": "fp32, seeded synthetic, resident in HBM",
             "l2": "inputs larger than the 126 MB L2; no flush between steps" if cfg.pixels * 4 > 126e6
-            else "L2 flushed (256 MB write) before every timed step",
-            "parallelism": ("row strips x%d, NCCL halo exchange" % world if cfg.name in ("1", "2", "3", "4", "4b")
+            else "L2 flushed before every timed step (256 MB read, outside the per-step CUDA events)",
+            "parallelism": ("row strips x%d, NCCL halo exchange per level" % world if cfg.name in ("1", "2", "3", "4", "4b")
                             and world > 1 else ("image shards x%d, no communication" % world if world > 1
                                                 else "single GPU"))}
 
@@ -153,7 +153,8 @@ class OursRunner:
         self.torch = torch
         self.flush = None
         if cfg.pixels * 4 <= 126e6:
-            self.flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)   # 256 MB
+            self.flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=device)   # 256 MB
+            self.flush_sink = torch.zeros((), dtype=torch.float32, device=device)
         self.launches = 0
         self.algo_bytes = 0           # algorithmic bytes one step moves on this rank
         self.level1_bytes = 0
@@ -189,35 +190,38 @@ class OursRunner:
             self.mode = "single"
             self.host_img = g.image(0)
         else:
-            if cfg.levels != 1:
-                raise SystemExit("row strips are one-level (multi-level strips: SURVEY 8f N3)")
+            # row strips, one ghost-row exchange per level (levels > 1: SURVEY 8f N3)
             g = cfg.groups[0]
             img = g.image(0)
-            self.ex = D.StripExchange(g.width, g.height, rank, world, device=device)
+            self.ex = D.StripPyramid(g.width, g.height, rank, world, cfg.levels, device=device)
             r0, r1 = self.ex.r0, self.ex.r1
-            self.ex.buf.copy_(torch.from_numpy(np.ascontiguousarray(
-                img[r0 - self.ex.ghost_top:r1 + self.ex.ghost_bot])))
-            self.splan = dwt2.StripPlan(g.width, g.height, r0, r1)
-            self.out = torch.empty((r1 - r0, g.width), dtype=torch.float32, device=device)
-            self.launches = 1 if self.overlap_off else 2
-            self.algo_bytes = BYTES_PER_PX * g.width * (r1 - r0)
-            self.level1_bytes = self.algo_bytes
+            self.ex.strip.copy_(torch.from_numpy(np.ascontiguousarray(img[r0:r1])))
+            self.splan = dwt2.StripPlan(g.width, g.height, r0, r1, cfg.levels)
+            self.out = self.ex.out
+            self.launches = cfg.levels * (1 if self.overlap_off else 2)
+            self.algo_bytes = sum(BYTES_PER_PX * w * (re - rb) for (w, h, rb, re, gt, gb) in self.ex.geom)
+            self.level1_bytes = BYTES_PER_PX * g.width * (r1 - r0)
             self.pixels = g.width * (r1 - r0)
             self.mode = "strip"
             self.host_img = img
 
     overlap_off = False
 
-    def step(self):
+    def flush_l2(self):
+        """Evict the L2 with clean lines: a read-only pass over 256 MB (a
+        write-based flush would leave ~126 MB of dirty lines whose write-back
+        lands in the next timed step)."""
         if self.flush is not None:
-            self.flush.zero_()
+            self.flush_sink.copy_(self.flush.amax())
+
+    def step(self):
         if self.mode == "single":
             self.plan.forward(self.x, self.out)
         elif self.mode == "batch":
             for plan, x, out in self.items:
                 plan.forward(x, out)
         else:
-            self.D.strip_forward_step(self.ex, self.splan, self.out, overlap=not self.overlap_off)
+            self.D.strip_pyramid_step(self.ex, self.splan, overlap=not self.overlap_off)
 
     def level1_kernel_ms(self, iters):
         """Average duration of the dominant kernel (level 1: 3/4 of the
@@ -238,8 +242,7 @@ class OursRunner:
         torch.cuda.synchronize()
         ts = []
         for _ in range(iters):
-            if self.flush is not None:
-                self.flush.zero_()
+            self.flush_l2()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
             for p, x, o in plans:
@@ -274,7 +277,7 @@ class OursRunner:
             s = torch.cuda.current_stream()
             def one():
                 self.ex.strip.copy_(hin, non_blocking=True)
-                self.D.strip_forward_step(self.ex, self.splan, self.out, overlap=True)
+                self.D.strip_pyramid_step(self.ex, self.splan, overlap=True)
                 hout.copy_(self.out, non_blocking=True)
             for _ in range(warm):
                 one()
@@ -423,26 +426,31 @@ def main():
     time.sleep(0.05)
     barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_host0 = time.perf_counter()
-    e0.record(stream)
-    for _ in range(args.steps):
-        do_step()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    if runner.flush is None:
+        # inputs larger than L2: K back-to-back steps between one event pair
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            do_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+    else:
+        # inputs that fit in L2: flush (untimed) before every step, one event
+        # pair around each step on the launching stream
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for a, b in evs:
+            runner.flush_l2()
+            a.record(stream)
+            do_step()
+            b.record(stream)
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
     t_host1 = time.perf_counter()
     barrier()
     sampler.stop()
-    ms = e0.elapsed_time(e1) / args.steps
-    if runner.flush is not None:
-        # subtract the L2-flush kernel, timed alone
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for _ in range(args.steps):
-            runner.flush.zero_()
-        f1.record(stream)
-        torch.cuda.synchronize()
-        ms -= f0.elapsed_time(f1) / args.steps
     ms_t = torch.tensor([ms], device=device)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)

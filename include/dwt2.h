@@ -96,6 +96,44 @@ dwt2_plan *dwt2_plan_create_batched(int32_t width, int32_t height, int32_t level
 dwt2_plan *dwt2_plan_create_strip(int32_t width, int32_t global_height, int32_t row_begin,
                                   int32_t row_end, int32_t boundary);
 
+/* Multi-level strip plan: `levels` levels of the row
+ * strip [row_begin, row_end) of a width x global_height image, one halo
+ * exchange per level.  row_begin must be a multiple of 2^levels, row_end a
+ * multiple of 2^levels or equal to global_height, and every level's strip
+ * must keep >= 2 rows.  Level k (0-based) transforms rows [rb_k, re_k) of
+ * the level-k input (the LL of level k-1), rb_k = row_begin / 2^k,
+ * re_k = ceil(re_{k-1} / 2); see dwt2_strip_level_info.  The plan owns no
+ * image buffers: the caller provides each level's ghost-padded input.
+ * dwt2_plan_create_strip is this with levels = 1. */
+dwt2_plan *dwt2_plan_create_strip_levels(int32_t width, int32_t global_height, int32_t row_begin,
+                                         int32_t row_end, int32_t levels, int32_t boundary);
+
+/* Geometry of level k of a strip plan: the level's global input size
+ * (width x global_height), the strip's rows [row_begin, row_end) of it, and
+ * the ghost rows its input buffer carries (2 above unless row_begin == 0,
+ * 1 below unless row_end == global_height). */
+typedef struct {
+    int32_t width, global_height, row_begin, row_end, ghost_top, ghost_bot;
+} dwt2_strip_level_t;
+
+int32_t dwt2_strip_level_info(const dwt2_plan *plan, int32_t level, dwt2_strip_level_t *info);
+
+/* Level k of a multi-level strip plan.
+ * in:     device, (ghost_top + rows + ghost_bot) x in_pitch fp32 (rows =
+ *         row_end - row_begin of level k; in_pitch >= the level width),
+ *         the ghost rows already filled (neighbour strips or exchange).
+ * ll_out: device, where the level's LL rows go ((rows + 1) / 2 rows, pitch
+ *         ll_pitch): the first owned row of level k+1's input buffer.
+ *         Ignored (may be NULL) for the last level, whose LL goes to out.
+ * out:    device, the strip-local Mallat pyramid: W x (row_end - row_begin)
+ *         of level 0, pitch W; level k writes its subband rows where a
+ *         Mallat pyramid of that W x h image puts level k.
+ * part:   as dwt2_forward_strip.
+ * in, out and ll_out must not overlap. */
+int32_t dwt2_forward_strip_level(const dwt2_plan *plan, int32_t level, const float *in, int64_t in_pitch,
+                                 float *ll_out, int64_t ll_pitch, float *out, int32_t part,
+                                 dwt2_stream_t stream);
+
 /* Forward transform of one image.
  * in:  device pointer, W x H fp32, row pitch W elements, caller-owned,
  *      read-only, 4-byte aligned.
@@ -111,7 +149,7 @@ int32_t dwt2_forward(const dwt2_plan *plan, const float *in, float *out, dwt2_st
 int32_t dwt2_forward_batched(const dwt2_plan *plan, const float *in, float *out, int32_t count,
                              int64_t in_stride, int64_t out_stride, dwt2_stream_t stream);
 
-/* Forward transform of a strip plan (see dwt2_plan_create_strip for the
+/* Forward transform of a one-level strip plan (see dwt2_plan_create_strip for the
  * `in` / `out` layouts).  part selects all quad rows, only the interior ones
  * (which read no ghost row, so they may run while the ghost rows are still in
  * flight) or only the two boundary quad rows. */

@@ -1049,7 +1049,7 @@ dwt2_plan *make_plan(int W, int H, int levels, int boundary, int max_count, bool
     p->scratch_bytes += cbytes;
     // LL scratch: level k (1-based, k < levels) writes LL_k to scratch[(k-1) % 2]
     for (int s = 0; s < 2; ++s) {
-        if (levels >= s + 2) {
+        if (!strip && levels >= s + 2) {   // strip plans: the caller owns every level's buffers
             const LevelGeom &g = p->geom[s];  // LL of level s+1
             p->sc_pitch[s] = round_up(g.Wq, 32);
             p->sc_img_stride[s] = p->sc_pitch[s] * g.Hq;
@@ -1192,19 +1192,6 @@ dwt2_plan *dwt2_plan_create_batched(int32_t width, int32_t height, int32_t level
     return make_plan(width, height, levels, boundary, max_count, false, height, 0, height);
 }
 
-dwt2_plan *dwt2_plan_create_strip(int32_t width, int32_t global_height, int32_t row_begin, int32_t row_end,
-                                  int32_t boundary)
-{
-    if (global_height < 2 || row_begin < 0 || row_begin >= row_end || row_end > global_height ||
-        (row_begin & 1) || ((row_end & 1) && row_end != global_height)) {
-        g_last_error = DWT2_EINVAL;
-        return nullptr;
-    }
-    // geometry is validated on the full image (every level input >= 2 x 2)
-    dwt2_plan *p = make_plan(width, global_height, 1, boundary, 1, true, global_height, row_begin, row_end);
-    return p;
-}
-
 int32_t dwt2_forward(const dwt2_plan *p, const float *in, float *out, dwt2_stream_t stream)
 {
     if (!p || !in || !out || p->strip || !aligned(in, 4) || !aligned(out, 4)) return fail(DWT2_EINVAL);
@@ -1236,35 +1223,106 @@ int32_t dwt2_forward_batched(const dwt2_plan *p, const float *in, float *out, in
     return DWT2_OK;
 }
 
-int32_t dwt2_forward_strip(const dwt2_plan *p, const float *in, float *out, int32_t part, dwt2_stream_t stream)
+dwt2_plan *dwt2_plan_create_strip_levels(int32_t width, int32_t global_height, int32_t row_begin, int32_t row_end,
+                                         int32_t levels, int32_t boundary)
 {
-    if (!p || !in || !out || !p->strip || part < 0 || part > 2 || !aligned(in, 4) || !aligned(out, 4))
+    if (levels < 1 || levels > 30 || global_height < 2 || row_begin < 0 || row_begin >= row_end ||
+        row_end > global_height) {
+        g_last_error = DWT2_EINVAL;
+        return nullptr;
+    }
+    const long long unit = 1LL << levels;
+    if ((row_begin % unit) != 0 || ((row_end % unit) != 0 && row_end != global_height)) {
+        g_last_error = DWT2_EINVAL;
+        return nullptr;
+    }
+    // geometry is validated on the full image (every level input >= 2 x 2)
+    dwt2_plan *p = make_plan(width, global_height, levels, boundary, 1, true, global_height, row_begin, row_end);
+    if (!p) return nullptr;
+    // every level's strip must hold >= 2 rows (the halo messages send 2 rows)
+    for (int k = 0; k < levels; ++k) {
+        dwt2_strip_level_t L;
+        dwt2_strip_level_info(p, k, &L);
+        if (L.row_end - L.row_begin < 2) {
+            dwt2_destroy(p);
+            g_last_error = DWT2_EINVAL;
+            return nullptr;
+        }
+    }
+    return p;
+}
+
+dwt2_plan *dwt2_plan_create_strip(int32_t width, int32_t global_height, int32_t row_begin, int32_t row_end,
+                                  int32_t boundary)
+{
+    return dwt2_plan_create_strip_levels(width, global_height, row_begin, row_end, 1, boundary);
+}
+
+int32_t dwt2_strip_level_info(const dwt2_plan *p, int32_t level, dwt2_strip_level_t *info)
+{
+    if (!p || !info || !p->strip || level < 0 || level >= p->levels) return fail(DWT2_EINVAL);
+    // rows [rb_k, re_k) of level k's input: rb_k = row_begin / 2^k, re_k = ceil(re_{k-1} / 2)
+    int rb = p->row_begin, re = p->row_end;
+    for (int k = 0; k < level; ++k) {
+        rb >>= 1;
+        re = (re + 1) >> 1;
+    }
+    const LevelGeom &g = p->geom[level];
+    info->width = g.W;
+    info->global_height = g.H;
+    info->row_begin = rb;
+    info->row_end = re;
+    info->ghost_top = rb > 0 ? 2 : 0;
+    info->ghost_bot = re < g.H ? 1 : 0;
+    return DWT2_OK;
+}
+
+int32_t dwt2_forward_strip_level(const dwt2_plan *p, int32_t level, const float *in, int64_t in_pitch,
+                                 float *ll_out, int64_t ll_pitch, float *out, int32_t part, dwt2_stream_t stream)
+{
+    dwt2_strip_level_t L;
+    if (!p || !in || !out || !p->strip || part < 0 || part > 2 || !aligned(in, 4) || !aligned(out, 4) ||
+        dwt2_strip_level_info(p, level, &L) != DWT2_OK || in_pitch < L.width)
         return fail(DWT2_EINVAL);
-    const int hl = p->row_end - p->row_begin;
-    const int in_rows = hl + p->ghost_top + p->ghost_bot;
-    const size_t in_bytes = size_t(p->W) * in_rows * sizeof(float);
-    const size_t out_bytes = size_t(p->W) * hl * sizeof(float);
+    const bool last = level == p->levels - 1;
+    if (!last && (!ll_out || !aligned(ll_out, 4) || ll_pitch < (L.width + 1) / 2)) return fail(DWT2_EINVAL);
+    const int rows = L.row_end - L.row_begin;
+    const int in_rows = rows + L.ghost_top + L.ghost_bot;
+    const int hloc0 = p->row_end - p->row_begin;          // strip-local pyramid: W x hloc0, pitch W
+    const size_t in_bytes = size_t(in_pitch) * in_rows * sizeof(float);
+    const size_t out_bytes = size_t(p->W) * hloc0 * sizeof(float);
     if (overlap(in, in_bytes, out, out_bytes) || !on_plan_device(p, in) || !on_plan_device(p, out))
         return fail(DWT2_EINVAL);
-    const int qs = p->row_begin / 2, qe = (p->row_end + 1) / 2;
+    if (!last) {
+        const size_t ll_bytes = size_t(ll_pitch) * ((rows + 1) / 2) * sizeof(float);
+        if (overlap(in, in_bytes, ll_out, ll_bytes) || overlap(out, out_bytes, ll_out, ll_bytes) ||
+            !on_plan_device(p, ll_out))
+            return fail(DWT2_EINVAL);
+    }
+    const int qs = L.row_begin / 2, qe = (L.row_end + 1) / 2;
     LaunchIO io;
     memset(&io, 0, sizeof(io));
     io.count = 1;
     io.in = in;
-    io.in_pitch = p->W;
-    io.in_img_stride = (long long)p->W * in_rows;
-    io.in_row0 = p->row_begin - p->ghost_top;
+    io.in_pitch = in_pitch;
+    io.in_img_stride = (long long)in_pitch * in_rows;
+    io.in_row0 = L.row_begin - L.ghost_top;
     io.in_rows = in_rows;
-    io.in_end = in + (long long)p->W * in_rows;
+    io.in_end = in + (long long)in_pitch * in_rows;
     io.out = out;
     io.out_pitch = p->W;
-    io.out_img_stride = (long long)p->W * hl;
+    io.out_img_stride = (long long)p->W * hloc0;
     io.out_q0 = qs;
     io.hq_local = qe - qs;
-    io.ll = out;
-    io.ll_pitch = p->W;
-    io.ll_img_stride = io.out_img_stride;
-    const int ia = qs + (p->ghost_top ? 1 : 0), ib = qe - (p->ghost_bot ? 1 : 0);
+    if (last) {
+        io.ll = out;
+        io.ll_pitch = p->W;
+    } else {
+        io.ll = ll_out;
+        io.ll_pitch = ll_pitch;
+    }
+    io.ll_img_stride = io.ll_pitch * (qe - qs);
+    const int ia = qs + (L.ghost_top ? 1 : 0), ib = qe - (L.ghost_bot ? 1 : 0);
     int a0, a1, b0 = 0, b1 = 0;
     if (part == DWT2_STRIP_ALL) {
         a0 = qs; a1 = qe;
@@ -1276,10 +1334,17 @@ int32_t dwt2_forward_strip(const dwt2_plan *p, const float *in, float *out, int3
         b0 = std::max(ib, ia); b1 = qe;
         if (b0 < a1) b0 = a1;
     }
-    int32_t r = launch_level(p, 0, p->W, p->Hg, io, a0, a1, b0, b1, reinterpret_cast<cudaStream_t>(stream));
+    int32_t r = launch_level(p, level, L.width, L.global_height, io, a0, a1, b0, b1,
+                             reinterpret_cast<cudaStream_t>(stream));
     if (r != DWT2_OK) return r;
     g_last_error = DWT2_OK;
     return DWT2_OK;
+}
+
+int32_t dwt2_forward_strip(const dwt2_plan *p, const float *in, float *out, int32_t part, dwt2_stream_t stream)
+{
+    if (!p || !p->strip || p->levels != 1) return fail(DWT2_EINVAL);
+    return dwt2_forward_strip_level(p, 0, in, p->W, nullptr, 0, out, part, stream);
 }
 
 int32_t dwt2_forward_host(const dwt2_plan *p, const float *host_in, float *host_out, dwt2_stream_t stream)
@@ -1396,7 +1461,13 @@ int32_t dwt2_plan_info(const dwt2_plan *p, dwt2_plan_info_t *info)
         const LevelGeom &g = p->geom[k];
         // level 1 reads the caller's buffer: TMA iff its rows are 16-byte aligned
         if (k > 0 || (p->W % 4) == 0) ++tma;
-        bytes += 8LL * g.W * (p->strip ? (p->row_end - p->row_begin) : g.H);
+        long long rows = g.H;
+        if (p->strip) {
+            dwt2_strip_level_t L;
+            dwt2_strip_level_info(p, k, &L);
+            rows = L.row_end - L.row_begin;
+        }
+        bytes += 8LL * g.W * rows;
     }
     info->tma_levels = tma;
     info->algorithmic_bytes = bytes;

@@ -14,6 +14,14 @@ while it is in flight (``DWT2_STRIP_INTERIOR``), then the two boundary quad
 rows (``DWT2_STRIP_BOUNDARY``).  The global top/bottom strips use the
 whole-sample symmetric mirror instead of ghosts.
 
+Multi-level strips: with L levels the strip bounds are
+multiples of 2^L (``strip_rows_levels``), so every level's strip is even-
+aligned in that level's LL image; each level exchanges its own ghost rows
+(2 above, 1 below) of the previous level's LL before its kernel runs
+(``StripPyramid``).  The strip-local output is the Mallat pyramid of the
+strip's W x rows sub-image, with every level's subband rows where a Mallat
+pyramid puts them.
+
 Batches (config 5) shard whole images with no communication.
 """
 from __future__ import annotations
@@ -27,6 +35,45 @@ def strip_rows(height: int, rank: int, world: int) -> tuple:
     lo = 2 * ((rank * hq) // world)
     hi = height if rank == world - 1 else 2 * (((rank + 1) * hq) // world)
     return lo, hi
+
+
+def strip_rows_levels(height: int, rank: int, world: int, levels: int = 1) -> tuple:
+    """[r_g, r_{g+1}) of rank g for an L-level pyramid: balanced runs of
+    2^L-row units (levels = 1 is ``strip_rows``)."""
+    unit = 1 << levels
+    nunits = -(-height // unit)
+    lo = unit * ((rank * nunits) // world)
+    hi = height if rank == world - 1 else unit * (((rank + 1) * nunits) // world)
+    return lo, hi
+
+
+def level_rows(width: int, height: int, lo: int, hi: int, levels: int) -> list:
+    """Per level k: (W_k, H_k, rb_k, re_k, ghost_top, ghost_bot) -- the level's
+    global input size and the strip's rows of it (rb_k = lo / 2^k,
+    re_k = ceil(re_{k-1} / 2)); mirrors dwt2_strip_level_info."""
+    out = []
+    w, h, rb, re = width, height, lo, hi
+    for _ in range(levels):
+        out.append((w, h, rb, re, 2 if rb > 0 else 0, 1 if re < h else 0))
+        w, h, rb, re = (w + 1) // 2, (h + 1) // 2, rb // 2, (re + 1) // 2
+    return out
+
+
+def halo_messages(rb: int, re: int, height: int, rank: int) -> list:
+    """The exchange of one level for rows [rb, re) of a `height`-row level
+    image (see ``halo_plan``)."""
+    gt, gb = (2 if rb > 0 else 0), (1 if re < height else 0)
+    n = re - rb
+    if n < 2:
+        raise ValueError("row strips need at least 2 rows per level")
+    msgs = []
+    if gt:
+        msgs.append(("recv", rank - 1, 0, 2))
+        msgs.append(("send", rank - 1, gt, 1))
+    if gb:
+        msgs.append(("recv", rank + 1, gt + n, 1))
+        msgs.append(("send", rank + 1, gt + n - 2, 2))
+    return msgs
 
 
 def shard(count: int, rank: int, world: int) -> range:
@@ -48,18 +95,7 @@ def halo_plan(height: int, rank: int, world: int) -> list:
       send its first strip row to rank-1 (their bottom ghost);
       send its last 2 strip rows to rank+1 (their top ghosts)."""
     lo, hi = strip_rows(height, rank, world)
-    gt, gb = ghost_rows(height, rank, world)
-    n = hi - lo
-    if n < 2:
-        raise ValueError("row strips need at least 2 rows each (H >= 2 G)")
-    msgs = []
-    if gt:
-        msgs.append(("recv", rank - 1, 0, 2))
-        msgs.append(("send", rank - 1, gt, 1))
-    if gb:
-        msgs.append(("recv", rank + 1, gt + n, 1))
-        msgs.append(("send", rank + 1, gt + n - 2, 2))
-    return msgs
+    return halo_messages(lo, hi, height, rank)
 
 
 def place_strip_output(full: np.ndarray, strip_out: np.ndarray, W: int, H: int, r0: int, r1: int) -> None:
@@ -130,3 +166,103 @@ def strip_forward_step(exchange: StripExchange, plan, out, overlap: bool = True,
         exchange.finish(reqs)
         plan.forward(exchange.buf, out, dwt2.DWT2_STRIP_ALL, stream)
     return out
+
+
+def _p2p(msgs, buf):
+    """Post grouped sends/receives of rows of `buf` (a 2-D tensor)."""
+    import torch.distributed as dist
+    ops = [dist.P2POp(dist.isend if op == "send" else dist.irecv, buf[row0:row0 + nrows], peer)
+           for op, peer, row0, nrows in msgs]
+    return dist.batch_isend_irecv(ops) if ops else []
+
+
+class StripPyramid:
+    """Rank's buffers of an L-level row-strip transform: one ghost-padded input
+    buffer per level (level 0: the image rows; level k >= 1: the LL of level
+    k-1, written by the level kernel into its owned rows) and the strip-local
+    output pyramid.  Row pitches of levels >= 1 are rounded up to 4 floats
+    (16-byte rows: the TMA-staged kernel path)."""
+
+    def __init__(self, width: int, height: int, rank: int, world: int, levels: int = 1, device=None):
+        import torch
+        self.width, self.height, self.rank, self.world, self.levels = width, height, rank, world, levels
+        self.r0, self.r1 = strip_rows_levels(height, rank, world, levels)
+        self.geom = level_rows(width, height, self.r0, self.r1, levels)
+        self.bufs = []
+        for k, (w, h, rb, re, gt, gb) in enumerate(self.geom):
+            pitch = width if k == 0 else -(-w // 4) * 4
+            full = torch.empty((gt + (re - rb) + gb, pitch), dtype=torch.float32, device=device)
+            self.bufs.append(full)
+        self.msgs = [halo_messages(rb, re, h, rank) for (w, h, rb, re, gt, gb) in self.geom]
+        self.out = torch.empty((self.r1 - self.r0, width), dtype=torch.float32, device=device)
+        self.ghost_top, self.ghost_bot = self.geom[0][4], self.geom[0][5]
+
+    @property
+    def buf(self):
+        return self.bufs[0]
+
+    def owned(self, k: int):
+        """Level k's owned rows (a view of its input buffer, level width)."""
+        w, h, rb, re, gt, gb = self.geom[k]
+        return self.bufs[k][gt:gt + (re - rb), :w]
+
+    @property
+    def strip(self):
+        return self.owned(0)
+
+    def level_buffer(self, k: int):
+        """Level k's whole ghost-padded buffer, level width columns."""
+        return self.bufs[k][:, :self.geom[k][0]]
+
+    def start(self, k: int):
+        """Post level k's ghost-row exchange over the default process group."""
+        return _p2p(self.msgs[k], self.bufs[k])
+
+    @staticmethod
+    def finish(reqs):
+        for r in reqs:
+            r.wait()
+
+    def global_rows(self, k: int) -> tuple:
+        """Global row range [lo, hi) of level k's buffer (ghosts included)."""
+        w, h, rb, re, gt, gb = self.geom[k]
+        return rb - gt, re + gb
+
+
+def strip_pyramid_step(pyr: StripPyramid, plan, overlap: bool = True, stream=None, exchange=None):
+    """All levels of rank's strip: per level, the ghost-row exchange and the
+    fused level kernel(s); with overlap, the interior quad rows run while the
+    ghost rows are in flight.  exchange(k) -> handle / finish(handle) may
+    replace the process-group exchange (single-GPU emulation in the tests)."""
+    from . import dwt2
+    for k in range(pyr.levels):
+        reqs = pyr.start(k) if exchange is None else exchange(k)
+        ll = pyr.owned(k + 1) if k + 1 < pyr.levels else None
+        buf = pyr.bufs[k]
+        if overlap:
+            plan.forward_level(k, buf, ll, pyr.out, dwt2.DWT2_STRIP_INTERIOR, stream)
+            if exchange is None:
+                pyr.finish(reqs)
+            plan.forward_level(k, buf, ll, pyr.out, dwt2.DWT2_STRIP_BOUNDARY, stream)
+        else:
+            if exchange is None:
+                pyr.finish(reqs)
+            plan.forward_level(k, buf, ll, pyr.out, dwt2.DWT2_STRIP_ALL, stream)
+    return pyr.out
+
+
+def place_pyramid_output(full: np.ndarray, strip_out: np.ndarray, W: int, H: int, r0: int, r1: int,
+                         levels: int) -> None:
+    """Copy a strip-local L-level pyramid (W x (r1-r0)) into the global one."""
+    w, h, rb, re, hl = W, H, r0, r1, r1 - r0
+    for k in range(levels):
+        Hq, Hh, Wq = (h + 1) // 2, h // 2, (w + 1) // 2
+        qs, qe = rb // 2, (re + 1) // 2
+        hq_loc = qe - qs
+        last = k == levels - 1
+        c0 = 0 if last else Wq                    # LL of inner levels is not output
+        full[qs:qe, c0:w] = strip_out[:hq_loc, c0:w]                          # (LL |) HL
+        h0, h1 = min(qs, Hh), min(qe, Hh)
+        if h1 > h0:
+            full[Hq + h0:Hq + h1, :w] = strip_out[hq_loc:hq_loc + (h1 - h0), :w]   # LH | HH
+        w, h, rb, re = Wq, Hq, qs, qe

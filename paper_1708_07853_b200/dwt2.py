@@ -27,6 +27,11 @@ _I32 = ctypes.c_int32
 _I64 = ctypes.c_int64
 
 
+class StripLevel(ctypes.Structure):
+    _fields_ = [("width", _I32), ("global_height", _I32), ("row_begin", _I32), ("row_end", _I32),
+                ("ghost_top", _I32), ("ghost_bot", _I32)]
+
+
 class PlanInfo(ctypes.Structure):
     _fields_ = [("width", _I32), ("height", _I32), ("levels", _I32), ("max_count", _I32),
                 ("launches_per_forward", _I32), ("tma_levels", _I32),
@@ -37,6 +42,9 @@ SIGNATURES = {
     "dwt2_plan_create": (_P, [_I32, _I32, _I32, _I32]),
     "dwt2_plan_create_batched": (_P, [_I32, _I32, _I32, _I32, _I32]),
     "dwt2_plan_create_strip": (_P, [_I32, _I32, _I32, _I32, _I32]),
+    "dwt2_plan_create_strip_levels": (_P, [_I32, _I32, _I32, _I32, _I32, _I32]),
+    "dwt2_strip_level_info": (_I32, [_P, _I32, ctypes.POINTER(StripLevel)]),
+    "dwt2_forward_strip_level": (_I32, [_P, _I32, _P, _I64, _P, _I64, _P, _I32, _P]),
     "dwt2_forward": (_I32, [_P, _P, _P, _P]),
     "dwt2_forward_batched": (_I32, [_P, _P, _P, _I32, _I64, _I64, _P]),
     "dwt2_forward_strip": (_I32, [_P, _P, _P, _I32, _P]),
@@ -110,6 +118,23 @@ def dwt2_plan_create_batched(width, height, levels, boundary, max_count):
 def dwt2_plan_create_strip(width, global_height, row_begin, row_end, boundary=DWT2_BOUNDARY_SYMMETRIC):
     return _plan_or_raise(lib().dwt2_plan_create_strip(width, global_height, row_begin, row_end, boundary),
                           "dwt2_plan_create_strip")
+
+
+def dwt2_plan_create_strip_levels(width, global_height, row_begin, row_end, levels,
+                                  boundary=DWT2_BOUNDARY_SYMMETRIC):
+    return _plan_or_raise(lib().dwt2_plan_create_strip_levels(width, global_height, row_begin, row_end, levels,
+                                                              boundary), "dwt2_plan_create_strip_levels")
+
+
+def dwt2_strip_level_info(plan, level) -> StripLevel:
+    info = StripLevel()
+    _check(lib().dwt2_strip_level_info(plan, level, ctypes.byref(info)), "dwt2_strip_level_info")
+    return info
+
+
+def dwt2_forward_strip_level(plan, level, in_ptr, in_pitch, ll_ptr, ll_pitch, out_ptr, part, stream):
+    _check(lib().dwt2_forward_strip_level(plan, level, in_ptr, in_pitch, ll_ptr, ll_pitch, out_ptr, part, stream),
+           "dwt2_forward_strip_level")
 
 
 def dwt2_forward(plan, in_ptr, out_ptr, stream):
@@ -258,23 +283,36 @@ class Plan:
 
 
 class StripPlan:
-    """One-level plan for the row strip [row_begin, row_end) of a W x Hg image."""
+    """Plan for the row strip [row_begin, row_end) of a W x Hg image, `levels`
+    levels with one halo exchange per level (levels = 1: config 3)."""
 
-    def __init__(self, width: int, global_height: int, row_begin: int, row_end: int):
-        self.width, self.global_height = width, global_height
+    def __init__(self, width: int, global_height: int, row_begin: int, row_end: int, levels: int = 1):
+        self.width, self.global_height, self.levels = width, global_height, levels
         self.row_begin, self.row_end = row_begin, row_end
-        self.ghost_top = 2 if row_begin > 0 else 0
-        self.ghost_bot = 1 if row_end < global_height else 0
-        self._p = dwt2_plan_create_strip(width, global_height, row_begin, row_end)
+        self._p = dwt2_plan_create_strip_levels(width, global_height, row_begin, row_end, levels)
+        self.level_info = [dwt2_strip_level_info(self._p, k) for k in range(levels)]
+        self.ghost_top = self.level_info[0].ghost_top
+        self.ghost_bot = self.level_info[0].ghost_bot
 
     @property
     def in_rows(self) -> int:
         return self.row_end - self.row_begin + self.ghost_top + self.ghost_bot
 
     def forward(self, x_with_ghosts, out, part=DWT2_STRIP_ALL, stream=None):
+        """One-level plans: level 0 from the ghost-padded strip (pitch W)."""
         _check_image(x_with_ghosts, "x")
         _check_image(out, "out")
         dwt2_forward_strip(self._p, x_with_ghosts.data_ptr(), out.data_ptr(), part, _stream_handle(stream))
+        return out
+
+    def forward_level(self, level, buf, ll_out, out, part=DWT2_STRIP_ALL, stream=None):
+        """Level `level`: buf = its ghost-padded input (2-D tensor, row pitch =
+        buf.stride(0)); ll_out = 2-D view of the next level's owned rows (None
+        for the last level); out = the strip-local pyramid (W x rows)."""
+        _check_image(out, "out")
+        ll_ptr, ll_pitch = (0, 0) if ll_out is None else (ll_out.data_ptr(), ll_out.stride(0))
+        dwt2_forward_strip_level(self._p, level, buf.data_ptr(), buf.stride(0), ll_ptr, ll_pitch, out.data_ptr(),
+                                 part, _stream_handle(stream))
         return out
 
     def close(self):

@@ -40,7 +40,8 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "scheme_compare.json"))
     args = ap.parse_args()
     torch.cuda.set_device(0)
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > L2
+    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > L2
+    sink = torch.zeros((), device="cuda")
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     rows = []
@@ -59,7 +60,7 @@ def main():
                 plan.forward_scheme(scheme, x, out)
             fg = torch.cuda.CUDAGraph()
             with torch.cuda.graph(fg):
-                flush.zero_()
+                sink.copy_(flush.amax())          # read-only: evicts L2 with clean lines
             for _ in range(3):
                 fg.replay()
                 g.replay()

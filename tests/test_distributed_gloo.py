@@ -113,3 +113,84 @@ def test_batch_shards_cover():
             for g in range(G):
                 seen.extend(D.shard(count, g, G))
             assert seen == list(range(count))
+
+
+# --------------------------------------------------------------------------
+# multi-level strips: one exchange per level
+# --------------------------------------------------------------------------
+
+def _level_image(W, H, k):
+    """Synthetic stand-in for level k's input (the exchange moves rows; their
+    values do not matter, only that every ghost row is the right global row)."""
+    return ((np.arange(H * W, dtype=np.float64).reshape(H, W) * (k + 3)) % 997.0).astype(np.float32)
+
+
+def _worker_levels(rank, world, port, W, H, L, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pyr = D.StripPyramid(W, H, rank, world, L, device="cpu")
+        oks = []
+        for k, (w, h, rb, re, gt, gb) in enumerate(pyr.geom):
+            img = _level_image(w, h, k)
+            pyr.bufs[k].fill_(-1.0)
+            pyr.owned(k).copy_(torch.from_numpy(img[rb:re]))
+            pyr.finish(pyr.start(k))
+            lo, hi = pyr.global_rows(k)
+            oks.append(bool(np.array_equal(pyr.level_buffer(k).numpy(), img[lo:hi])))
+        q.put((rank, oks, pyr.r0, pyr.r1))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,W,H,L", [(2, 40, 64, 3), (3, 33, 97, 2), (3, 20, 130, 4)])
+def test_multilevel_strip_exchange_gloo(world, W, H, L):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_levels, args=(r, world, port, W, H, L, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, oks, r0, r1 in res:
+        assert all(oks), f"rank {rank}: ghost rows wrong at levels {[k for k, o in enumerate(oks) if not o]}"
+    assert res[0][2] == 0 and res[-1][3] == H
+    for a, b in zip(res, res[1:]):
+        assert a[3] == b[2] and a[3] % (1 << L) == 0
+
+
+def test_multilevel_partition_and_geometry():
+    for H in [64, 97, 130, 8193, 16384]:
+        for G in [1, 2, 3, 8]:
+            for L in [1, 2, 3, 8]:
+                unit = 1 << L
+                if -(-H // unit) < G:
+                    continue
+                prev = 0
+                for g in range(G):
+                    r0, r1 = D.strip_rows_levels(H, g, G, L)
+                    assert r0 == prev and r0 % unit == 0 and (r1 % unit == 0 or r1 == H)
+                    prev = r1
+                    geom = D.level_rows(64, H, r0, r1, L)
+                    # each level's strips tile that level's image
+                    for k, (w, h, rb, re, gt, gb) in enumerate(geom):
+                        assert rb == r0 >> k and rb % 2 == 0
+                        assert gt == (2 if rb else 0) and gb == (1 if re < h else 0)
+                assert prev == H
+
+
+def test_place_pyramid_output_tiles_global():
+    """Strip-local pyramids placed per rank rebuild the global Mallat pyramid
+    (every element written exactly once) -- checked on index maps."""
+    for W, H, G, L in [(24, 64, 2, 3), (17, 97, 3, 2), (40, 130, 3, 4)]:
+        cover = np.zeros((H, W), np.int32)
+        for g in range(G):
+            r0, r1 = D.strip_rows_levels(H, g, G, L)
+            mark = np.zeros((H, W), np.int32)
+            D.place_pyramid_output(mark, np.ones((r1 - r0, W), np.int32), W, H, r0, r1, L)
+            cover += mark
+        assert (cover == 1).all(), np.argwhere(cover != 1)[:5]
