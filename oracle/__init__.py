@@ -19,6 +19,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "dwt53_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "dwt97_oracle.c")]
 _LIB = os.path.join(_HERE, "liboracle_dwt53.so")
 _lib = None
 
@@ -27,11 +28,11 @@ BANDS = {"LL": 0, "HL": 1, "LH": 2, "HH": 3}
 
 def build(force: bool = False) -> str:
     """Compile the oracle shared library (idempotent)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(f) for f in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(
             ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c99", "-Wall",
-             "-shared", "-fPIC", _SRC, "-o", tmp])
+             "-shared", "-fPIC", *_SRCS, "-o", tmp])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -56,6 +57,13 @@ def _load():
         lib.oracle_dwt53_inv_lifting.restype = L
         lib.oracle_dwt53_conv_sample_f32.argtypes = [fp, L, L, L, L, ip, lp, lp, dp]
         lib.oracle_dwt53_conv_sample.argtypes = [dp, L, L, L, L, ip, lp, lp, dp]
+        lib.oracle_dwt97_fwd_1d.argtypes = [dp, L, dp]
+        lib.oracle_dwt97_inv_1d.argtypes = [dp, L, dp]
+        lib.oracle_dwt97_forward.argtypes = [dp, dp, L, L, L, ctypes.c_int, ctypes.c_int]
+        lib.oracle_dwt97_forward.restype = L
+        lib.oracle_dwt97_inverse.argtypes = [dp, dp, L, L, L, ctypes.c_int]
+        lib.oracle_dwt97_inverse.restype = L
+        lib.oracle_dwt97_conv_sample_f32.argtypes = [fp, L, L, L, L, ip, lp, lp, dp]
         lib.oracle_wss_index.argtypes = [L, L]
         lib.oracle_wss_index.restype = L
         _lib = lib
@@ -81,9 +89,26 @@ def inv_1d(c) -> np.ndarray:
     return out
 
 
-def forward(img, levels: int = 1, round_f32: bool = False, algorithm: str = "lifting") -> np.ndarray:
-    """Multi-level forward 2-D CDF 5/3 DWT of a H x W image, Mallat pyramid, fp64.
+def fwd_1d_97(x) -> np.ndarray:
+    """1-D forward CDF 9/7 lifting: [low (ceil(n/2)), high (floor(n/2))]."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    _load().oracle_dwt97_fwd_1d(_dptr(x), x.size, _dptr(out))
+    return out
 
+
+def inv_1d_97(c) -> np.ndarray:
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    out = np.empty_like(c)
+    _load().oracle_dwt97_inv_1d(_dptr(c), c.size, _dptr(out))
+    return out
+
+
+def forward(img, levels: int = 1, round_f32: bool = False, algorithm: str = "lifting",
+            wavelet: str = "cdf53") -> np.ndarray:
+    """Multi-level forward 2-D DWT of a H x W image, Mallat pyramid, fp64.
+
+    wavelet: "cdf53" (dwt53_oracle.c) or "cdf97" (dwt97_oracle.c).
     algorithm: "lifting" (A, separable lifting) or "conv" (B, brute force).
     round_f32: round every level's output to fp32 before the next level
     (oracle output (ii) in DESIGN.md; False gives output (i)).
@@ -91,25 +116,30 @@ def forward(img, levels: int = 1, round_f32: bool = False, algorithm: str = "lif
     img = np.ascontiguousarray(img, dtype=np.float64)
     H, W = img.shape
     out = np.empty_like(img)
-    fn = _load().oracle_dwt53_fwd_lifting if algorithm == "lifting" else _load().oracle_dwt53_fwd_conv
-    r = fn(_dptr(img), _dptr(out), W, H, levels, int(bool(round_f32)))
+    if wavelet == "cdf97":
+        r = _load().oracle_dwt97_forward(_dptr(img), _dptr(out), W, H, levels, int(bool(round_f32)),
+                                         int(algorithm == "conv"))
+    else:
+        fn = _load().oracle_dwt53_fwd_lifting if algorithm == "lifting" else _load().oracle_dwt53_fwd_conv
+        r = fn(_dptr(img), _dptr(out), W, H, levels, int(bool(round_f32)))
     if r < 0:
         raise ValueError("oracle: invalid arguments")
     return out
 
 
-def inverse(coeffs, levels: int = 1, round_f32: bool = False) -> np.ndarray:
+def inverse(coeffs, levels: int = 1, round_f32: bool = False, wavelet: str = "cdf53") -> np.ndarray:
     """Multi-level inverse (algorithm C) of a Mallat pyramid, fp64.
     round_f32: round every level's reconstruction to fp32 (the GPU storage type)."""
     c = np.ascontiguousarray(coeffs, dtype=np.float64)
     H, W = c.shape
     out = np.empty_like(c)
-    if _load().oracle_dwt53_inv_lifting(_dptr(c), _dptr(out), W, H, levels, int(bool(round_f32))) < 0:
+    fn = _load().oracle_dwt97_inverse if wavelet == "cdf97" else _load().oracle_dwt53_inv_lifting
+    if fn(_dptr(c), _dptr(out), W, H, levels, int(bool(round_f32))) < 0:
         raise ValueError("oracle: invalid arguments")
     return out
 
 
-def conv_sample(img, band, m, n) -> np.ndarray:
+def conv_sample(img, band, m, n, wavelet: str = "cdf53") -> np.ndarray:
     """Pointwise brute-force convolution (algorithm B) of one level.
 
     img: H x W array (fp32 or fp64; rows may have a pitch >= W via a 2-D view
@@ -127,7 +157,12 @@ def conv_sample(img, band, m, n) -> np.ndarray:
     ip = band.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
     mp = m.ctypes.data_as(ctypes.POINTER(ctypes.c_long))
     nq = n.ctypes.data_as(ctypes.POINTER(ctypes.c_long))
-    if img.dtype == np.float32:
+    if wavelet == "cdf97":
+        if img.dtype != np.float32:
+            raise TypeError("cdf97 samples: fp32 images")
+        lib.oracle_dwt97_conv_sample_f32(img.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                         pitch, W, H, band.size, ip, mp, nq, _dptr(res))
+    elif img.dtype == np.float32:
         lib.oracle_dwt53_conv_sample_f32(img.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
                                          pitch, W, H, band.size, ip, mp, nq, _dptr(res))
     elif img.dtype == np.float64:

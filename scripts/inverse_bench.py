@@ -26,16 +26,19 @@ def timed(fn, flush, iters):
     for _ in range(3):
         g.replay()
     torch.cuda.synchronize()
-    ts = []
-    for _ in range(iters):
-        if flush is not None:
-            flush.amax()                  # read-only pass: evicts L2 with clean lines
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        g.replay()
-        e1.record()
-        e1.synchronize()
-        ts.append(e0.elapsed_time(e1) * 1e3)
+    # K (flush + call) back to back minus K flushes alone (event ticks are 2.048 us)
+    def run(k, with_call):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(k):
+            if flush is not None:
+                flush.amax()
+            if with_call:
+                g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) * 1e3
+    ts = [(run(iters, True) - run(iters, False)) / iters for _ in range(5)]
     return statistics.median(ts)
 
 

@@ -65,15 +65,23 @@ def main():
                 fg.replay()
                 g.replay()
             torch.cuda.synchronize()
+            # K (flush + call) back to back minus K flushes alone: CUDA event
+            # timestamps tick every 2.048 us here (scripts/diag_small.py)
             ts = []
-            for _ in range(args.iters):
-                fg.replay()
+            for _ in range(5):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                g.replay()
+                for _ in range(args.iters):
+                    fg.replay()
+                    g.replay()
                 e1.record()
-                e1.synchronize()
-                ts.append(e0.elapsed_time(e1) * 1e3)
+                f0.record()
+                for _ in range(args.iters):
+                    fg.replay()
+                f1.record()
+                torch.cuda.synchronize()
+                ts.append((e0.elapsed_time(e1) - f0.elapsed_time(f1)) * 1e3 / args.iters)
             us = statistics.median(ts)
             px = edge * edge
             r = {"edge": edge, "scheme": scheme, "paper": PAPER[scheme],
