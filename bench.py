@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="3", choices=["1", "2", "3", "4", "4b", "5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--wavelet", default="cdf53", choices=["cdf53", "cdf97"],
+                    help="cdf97: the K = 2 non-separable kernel (SURVEY 8f N4); single-image and batch configs")
     ap.add_argument("--no-overlap", action="store_true", help="strips: exchange, then one launch")
     ap.add_argument("--no-graph", action="store_true", help="launch every step from the host instead of "
                     "replaying a CUDA graph of it")
@@ -134,8 +136,9 @@ def describe(cfg, world):
         images = f"{g0.width}x{g0.height}"
     return {"workload": f"config {cfg.name}: {cfg.description}", "images": images, "levels": cfg.levels,
             "pixels": cfg.pixels, "input": "fp32, seeded synthetic, resident in HBM",
-            "l2": "inputs larger than the 126 MB L2; no flush between steps" if cfg.pixels * 4 > 126e6
-            else "L2 flushed before every timed step (256 MB read pass; K flushes timed alone and subtracted)",
+            "l2": "inputs larger than the 126 MB L2; no flush between steps" if cfg.pixels * 8 >= 2 * 126e6
+            else "each of the K timed steps reads its own input buffer (K distinct input/output pairs); L2 "
+                 "flushed (256 MB read pass) once before the timed region",
             "parallelism": ("row strips x%d, NCCL halo exchange per level" % world if cfg.name in ("1", "2", "3", "4", "4b")
                             and world > 1 else ("image shards x%d, no communication" % world if world > 1
                                                 else "single GPU"))}
@@ -152,9 +155,15 @@ class OursRunner:
         self.dwt2, self.D = dwt2, D
         self.torch = torch
         self.flush = None
-        if cfg.pixels * 4 <= 126e6:
+        # inputs + outputs smaller than 2x the 126 MB L2: every timed step gets
+        # its own input/output pair (K distinct pairs) and the L2 is flushed
+        # once (read-only pass) before the timed region
+        self.small = cfg.pixels * 8 < 2 * 126e6
+        if self.small:
             self.flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=device)   # 256 MB
             self.flush_sink = torch.zeros((), dtype=torch.float32, device=device)
+        self.nbuf = max(1, self.steps) if self.small else 1
+        self.i = 0
         self.launches = 0
         self.algo_bytes = 0           # algorithmic bytes one step moves on this rank
         self.level1_bytes = 0
@@ -169,7 +178,7 @@ class OursRunner:
                 xs = np.stack([grp.image(i) for i in idx])
                 x = torch.from_numpy(xs).to(device)
                 out = torch.empty_like(x)
-                plan = dwt2.Plan(grp.width, grp.height, cfg.levels, max_count=len(idx))
+                plan = dwt2.Plan(grp.width, grp.height, cfg.levels, max_count=len(idx), wavelet=self.wavelet)
                 info = plan.info()
                 self.items.append((plan, x, out))
                 self.launches += info.launches_per_forward
@@ -180,8 +189,10 @@ class OursRunner:
         elif world == 1:
             g = cfg.groups[0]
             x = torch.from_numpy(g.image(0)).to(device)
-            self.x, self.out = x, torch.empty_like(x)
-            self.plan = dwt2.Plan(g.width, g.height, cfg.levels)
+            self.xs = [x] + [x.clone() for _ in range(self.nbuf - 1)]
+            self.outs = [torch.empty_like(x) for _ in range(self.nbuf)]
+            self.x, self.out = x, self.outs[0]
+            self.plan = dwt2.Plan(g.width, g.height, cfg.levels, wavelet=self.wavelet)
             info = self.plan.info()
             self.launches = info.launches_per_forward
             self.algo_bytes = info.algorithmic_bytes
@@ -206,6 +217,8 @@ class OursRunner:
             self.host_img = img
 
     overlap_off = False
+    wavelet = "cdf53"
+    steps = 20
 
     def flush_l2(self):
         """Evict the L2 with clean lines: a read-only pass over 256 MB (a
@@ -216,7 +229,9 @@ class OursRunner:
 
     def step(self):
         if self.mode == "single":
-            self.plan.forward(self.x, self.out)
+            j = self.i % self.nbuf
+            self.i += 1
+            self.plan.forward(self.xs[j], self.outs[j])
         elif self.mode == "batch":
             for plan, x, out in self.items:
                 plan.forward(x, out)
@@ -234,9 +249,11 @@ class OursRunner:
         if self.mode == "strip":
             return None
         if self.mode == "single":
-            plans = [(self.dwt2.Plan(self.cfg.groups[0].width, self.cfg.groups[0].height, 1), self.x, self.out)]
+            plans = [(self.dwt2.Plan(self.cfg.groups[0].width, self.cfg.groups[0].height, 1, wavelet=self.wavelet),
+                       self.x, self.out)]
         else:
-            plans = [(self.dwt2.Plan(p.width, p.height, 1, max_count=x.shape[0]), x, o) for p, x, o in self.items]
+            plans = [(self.dwt2.Plan(p.width, p.height, 1, max_count=x.shape[0], wavelet=self.wavelet), x, o)
+                     for p, x, o in self.items]
         for p, x, o in plans:          # warm-up (tensor maps, first-launch costs)
             p.forward(x, o)
         torch.cuda.synchronize()
@@ -404,6 +421,10 @@ def main():
         dist.init_process_group("nccl", device_id=device)
 
     OursRunner.overlap_off = args.no_overlap
+    OursRunner.steps = args.steps
+    OursRunner.wavelet = args.wavelet
+    if args.wavelet != "cdf53" and world > 1 and cfg.name != "5":
+        raise SystemExit("row strips run the CDF 5/3 kernel only")
     runner = OursRunner(cfg, rank, world, device)
     stream = torch.cuda.current_stream()
 
@@ -416,50 +437,36 @@ def main():
     torch.cuda.synchronize()
     graph = None
     if not args.no_graph and runner.mode != "strip":
-        # one step as a CUDA graph (the level kernels keep their programmatic
-        # dependent-launch edges); replaying it removes host launch gaps
+        # the K timed steps as ONE CUDA graph (the level kernels keep their
+        # programmatic dependent-launch edges): no host launch gaps, and the
+        # NVML sampler thread cannot gate the GPU
+        runner.i = 0
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            runner.step()
-        for _ in range(3):
-            graph.replay()
+            for _ in range(args.steps):
+                runner.step()
+        graph.replay()
         torch.cuda.synchronize()
-    do_step = graph.replay if graph is not None else runner.step
 
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.05)
+    if runner.small:
+        runner.flush_l2()
     barrier()
     torch.cuda.synchronize()
     t_host0 = time.perf_counter()
-    if runner.flush is None:
-        # inputs larger than L2: K back-to-back steps between one event pair
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            do_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / args.steps
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    if graph is not None:
+        graph.replay()
     else:
-        # inputs that fit in L2: a read-only L2 flush before every step.  CUDA
-        # event timestamps on this driver tick every 2.048 us (measured,
-        # scripts/diag_small.py), so small steps are not bracketed one by
-        # one: K (flush + step) pairs are timed back to back, then K flushes
-        # alone, and the difference is the K steps.
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        runner.i = 0
         for _ in range(args.steps):
-            runner.flush_l2()
-            do_step()
-        e1.record(stream)
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for _ in range(args.steps):
-            runner.flush_l2()
-        f1.record(stream)
-        torch.cuda.synchronize()
-        ms = (e0.elapsed_time(e1) - f0.elapsed_time(f1)) / args.steps
+            runner.step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
     t_host1 = time.perf_counter()
     barrier()
     sampler.stop()
@@ -503,22 +510,24 @@ def main():
         algo_bytes_total = runner.algo_bytes * world if cfg.name != "5" else sum(
             BYTES_PER_PX * workloads.level_pixels(g.width, g.height, cfg.levels) * g.count for g in cfg.groups)
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if args.wavelet == "cdf53" else METRIC.replace("CDF 5/3", "CDF 9/7"),
+            "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "weak" if cfg.name == "5" else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": describe(cfg, world),
+            "config": dict(describe(cfg, world), **({"wavelet": args.wavelet} if args.wavelet != "cdf53" else {})),
             "hbm_gbs_algorithmic": algo_bytes_total / (ms_max * 1e-3) / 1e9,
             "ns_per_pel": ms_max * 1e6 / total_px,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "dwt53_level_kernel (level 1)", "kernel_ms": k_ms,
+                         "kernel": ("dwt53_level_kernel" if args.wavelet == "cdf53" else "dwt_k2_level_kernel")
+                         + " (level 1)", "kernel_ms": k_ms,
                          "bytes_per_launch": k_bytes, "peak_source": peak_src,
                          "frac_of_8tbs": achieved / 8000.0},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": runner.launches * args.steps,
-            "launch": "CUDA graph replay of one step" if graph is not None else "host launches",
+            "launch": "one CUDA graph of the K timed steps" if graph is not None else "host launches",
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

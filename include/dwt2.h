@@ -67,6 +67,16 @@ enum {
 
 enum { DWT2_BOUNDARY_SYMMETRIC = 0 }; /* whole-sample symmetric extension */
 
+/* Wavelets (dwt2_plan_create_ex).  The paper evaluates CDF 5/3
+ * and states the schemes are general (L39, L365-367). */
+enum {
+    DWT2_WAVELET_CDF53 = 0,    /* CDF 5/3, the fused non-separable kernel (the product path) */
+    DWT2_WAVELET_CDF97 = 1,    /* CDF 9/7: Eq. (5) for K = 2 lifting pairs + scaling, one fused kernel per
+                                  level; constants of Daubechies & Sweldens, JPEG 2000 normalisation
+                                  (low / K, high * K; DESIGN.md C-B1..C-B3) */
+    DWT2_WAVELET_CDF53_K2 = 2  /* CDF 5/3 through the K = 2 kernel (second pair = 0, K = 1): a cross-check */
+};
+
 enum {                         /* dwt2_forward_strip `part` */
     DWT2_STRIP_ALL = 0,        /* every quad row of the strip */
     DWT2_STRIP_INTERIOR = 1,   /* quad rows that read no ghost row */
@@ -78,6 +88,14 @@ enum {                         /* dwt2_forward_strip `part` */
  * Allocates and owns the LL scratch of levels >= 2 on the current device.
  * Returns NULL on error (dwt2_last_error()). */
 dwt2_plan *dwt2_plan_create(int32_t width, int32_t height, int32_t levels, int32_t boundary);
+
+/* General plan: `wavelet` (DWT2_WAVELET_*), up to max_count images per
+ * batched call.  Plans of a wavelet other than CDF53 support dwt2_forward and
+ * dwt2_forward_batched only (others return DWT2_EUNSUPPORTED); their
+ * arithmetic is fp64 in registers, fp32 in memory, so results match the
+ * fp64 definition within fp32 rounding of each level's output. */
+dwt2_plan *dwt2_plan_create_ex(int32_t width, int32_t height, int32_t levels, int32_t boundary, int32_t wavelet,
+                               int32_t max_count);
 
 /* As dwt2_plan_create, with scratch for up to max_count images per
  * dwt2_forward_batched call (BASELINE.json config 5). */

@@ -1,7 +1,7 @@
 """Compile the CUDA library in-tree for sm_100a (used by __graft_entry__.build()).
 
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared -Xcompiler -fPIC
-  csrc/{dwt2,inverse,schemes}.cu -> paper_1708_07853_b200/libdwt2.so   (links only cudart; the TMA
+  csrc/{dwt2,inverse,schemes,dwt97}.cu -> paper_1708_07853_b200/libdwt2.so   (links only cudart; the TMA
 descriptor encoder is fetched from the driver at run time).
 """
 from __future__ import annotations
@@ -11,7 +11,7 @@ import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-SRCS = [os.path.join(PKG, "csrc", f) for f in ("dwt2.cu", "inverse.cu", "schemes.cu")]
+SRCS = [os.path.join(PKG, "csrc", f) for f in ("dwt2.cu", "inverse.cu", "schemes.cu", "dwt97.cu")]
 DEPS = SRCS + [os.path.join(PKG, "csrc", "dwt2_internal.h")]
 HDR = os.path.join(ROOT, "include", "dwt2.h")
 LIB = os.path.join(PKG, "libdwt2.so")

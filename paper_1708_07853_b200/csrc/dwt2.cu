@@ -79,7 +79,7 @@ namespace {
 #define DWT2_MINB 4
 #endif
 #ifndef DWT2_MIN_TPW
-#define DWT2_MIN_TPW 2
+#define DWT2_MIN_TPW 6                // below this many tiles per warp: one static tile per warp (c2 sweep)
 #endif
 #ifndef DWT2_TPW
 #define DWT2_TPW 32                 // target tiles per warp on large levels (measured optimum)
@@ -980,8 +980,13 @@ int32_t configure_kernels(int *max_ctas)
     return status;
 }
 
-dwt2_plan *make_plan(int W, int H, int levels, int boundary, int max_count, bool strip, int Hg, int rb, int re)
+dwt2_plan *make_plan(int W, int H, int levels, int boundary, int max_count, bool strip, int Hg, int rb, int re,
+                     int wavelet = DWT2_WAVELET_CDF53)
 {
+    if (wavelet < DWT2_WAVELET_CDF53 || wavelet > DWT2_WAVELET_CDF53_K2 || (strip && wavelet != DWT2_WAVELET_CDF53)) {
+        g_last_error = wavelet < 0 || wavelet > DWT2_WAVELET_CDF53_K2 ? DWT2_EINVAL : DWT2_EUNSUPPORTED;
+        return nullptr;
+    }
     if (boundary != DWT2_BOUNDARY_SYMMETRIC) {
         g_last_error = DWT2_EUNSUPPORTED;
         return nullptr;
@@ -1011,6 +1016,7 @@ dwt2_plan *make_plan(int W, int H, int levels, int boundary, int max_count, bool
     p->H = H;
     p->levels = levels;
     p->max_count = max_count;
+    p->wavelet = wavelet;
     p->device = dev;
     p->sms = prop.multiProcessorCount;
     p->strip = strip;
@@ -1186,6 +1192,12 @@ dwt2_plan *dwt2_plan_create(int32_t width, int32_t height, int32_t levels, int32
     return make_plan(width, height, levels, boundary, 1, false, height, 0, height);
 }
 
+dwt2_plan *dwt2_plan_create_ex(int32_t width, int32_t height, int32_t levels, int32_t boundary, int32_t wavelet,
+                               int32_t max_count)
+{
+    return make_plan(width, height, levels, boundary, max_count, false, height, 0, height, wavelet);
+}
+
 dwt2_plan *dwt2_plan_create_batched(int32_t width, int32_t height, int32_t levels, int32_t boundary,
                                     int32_t max_count)
 {
@@ -1198,6 +1210,12 @@ int32_t dwt2_forward(const dwt2_plan *p, const float *in, float *out, dwt2_strea
     const size_t bytes = size_t(p->W) * p->H * sizeof(float);
     if (overlap(in, bytes, out, bytes) || !on_plan_device(p, in) || !on_plan_device(p, out))
         return fail(DWT2_EINVAL);
+    if (p->wavelet != DWT2_WAVELET_CDF53) {
+        int32_t r = run_levels_k2(p, in, out, 1, (long long)p->W * p->H, (long long)p->W * p->H,
+                                  reinterpret_cast<cudaStream_t>(stream));
+        if (r == DWT2_OK) g_last_error = DWT2_OK;
+        return r;
+    }
     int32_t r = run_levels(p, in, out, 1, (long long)p->W * p->H, (long long)p->W * p->H, 0, p->levels - 1, 0,
                            p->geom[0].Hq, reinterpret_cast<cudaStream_t>(stream));
     if (r != DWT2_OK) return r;
@@ -1216,6 +1234,11 @@ int32_t dwt2_forward_batched(const dwt2_plan *p, const float *in, float *out, in
     const size_t out_bytes = size_t((count - 1) * out_stride + img) * sizeof(float);
     if (overlap(in, in_bytes, out, out_bytes) || !on_plan_device(p, in) || !on_plan_device(p, out))
         return fail(DWT2_EINVAL);
+    if (p->wavelet != DWT2_WAVELET_CDF53) {
+        int32_t r = run_levels_k2(p, in, out, count, in_stride, out_stride, reinterpret_cast<cudaStream_t>(stream));
+        if (r == DWT2_OK) g_last_error = DWT2_OK;
+        return r;
+    }
     int32_t r = run_levels(p, in, out, count, in_stride, out_stride, 0, p->levels - 1, 0, p->geom[0].Hq,
                            reinterpret_cast<cudaStream_t>(stream));
     if (r != DWT2_OK) return r;
@@ -1350,6 +1373,7 @@ int32_t dwt2_forward_strip(const dwt2_plan *p, const float *in, float *out, int3
 int32_t dwt2_forward_host(const dwt2_plan *p, const float *host_in, float *host_out, dwt2_stream_t stream)
 {
     if (!p || !host_in || !host_out || p->strip || p->max_count != 1) return fail(DWT2_EINVAL);
+    if (p->wavelet != DWT2_WAVELET_CDF53) return fail(DWT2_EUNSUPPORTED);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const long long npx = (long long)p->W * p->H;
     if (!p->d_in) {

@@ -42,6 +42,7 @@ inline bool overlap(const void *a, size_t an, const void *b, size_t bn)
 
 struct dwt2_plan {
     int W, H, levels, max_count;
+    int wavelet;              // DWT2_WAVELET_*: CDF53 runs the fused 5/3 kernel (dwt2.cu), others dwt97.cu
     int device;
     // strip plans
     bool strip;
@@ -80,5 +81,9 @@ namespace dwt2_detail {
 
 // true if ptr is device (or managed) memory of the plan's device (cached)
 bool on_plan_device(const dwt2_plan *p, const void *ptr);
+
+// all levels through the K = 2 lifting kernel (dwt97.cu)
+int32_t run_levels_k2(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,
+                      long long out_stride, cudaStream_t s);
 
 }  // namespace dwt2_detail

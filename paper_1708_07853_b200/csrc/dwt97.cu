@@ -1,0 +1,453 @@
+// dwt97.cu -- B200 (sm_100a) forward 2-D CDF 9/7 DWT with the non-separable
+// lifting scheme of arXiv:1708.07853 generalised to K = 2 lifting pairs
+// ("the presented
+// schemes are general and they are not limited to any particular wavelet").
+//
+// Eq. (5) with the pair (P_k, U_k) = (c_{2k} (1 + z),
+// c_{2k+1} (1 + z^-1)) is applied for k = 1, 2 -- four spatial steps
+// (predict 1 | update 1 | predict 2 | update 2) instead of the eight of the
+// separable lifting scheme -- followed by the 2-D scaling of the subbands
+// (LL / K^2, HL and LH * 1, HH * K^2).  CDF 9/7: (c0, c1, c2, c3) = (alpha,
+// beta, gamma, delta) of Daubechies & Sweldens with JPEG 2000 normalisation
+// (readings C-B1..C-B3).  The same kernel runs the CDF 5/3 pair as
+// (-1/2, 1/4, 0, 0), K = 1 (a cross-check against the 5/3 path).
+//
+// One fused kernel per level, no intermediate ever leaves the registers:
+// a warp owns a slab of 64 quad columns of which the middle 60 are output
+// (lanes 1..30; lanes 0 and 31 carry the 2-quad halo each side that the four
+// steps need) and walks DOWN it one quad row at a time.  Each spatial step
+// reads its vertical neighbours from rows carried in registers (the predicts
+// look one row ahead, the updates one row back, so the output lags the input
+// by two quad rows) and its horizontal neighbours from the adjacent lane by
+// shuffle.  The paper's synchronisation points `|` are
+// warp shuffles.
+//
+// Boundaries: whole-sample symmetric extension applied to the PIXELS as they
+// are loaded (every index mirrored), so every tile transforms the extended
+// image and no quad-domain boundary rule is needed -- the same definition
+// the oracle computes (oracle/dwt97_oracle.c, "transform of the symmetric
+// extension").  fp32 in HBM, fp64 in registers.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "dwt2_internal.h"
+
+using namespace dwt2_detail;
+
+namespace {
+
+constexpr int KW = 4;                      // warps per CTA
+constexpr int KT = KW * 32;
+constexpr int SLABQ = 64;                  // quad columns per warp (2 per lane)
+constexpr int OUTQ = 60;                   // output quad columns per warp (lanes 1..30)
+constexpr int DS = 8;                      // raw quad rows in flight per warp (shared-memory ring, cp.async)
+constexpr int DR = 1;                      // raw quad rows in flight per warp on the register path (edge slabs)
+constexpr size_t K2_SMEM = size_t(KW) * DS * 2 * 128 * sizeof(float);
+
+__device__ __forceinline__ void cp_async16(float *dst, const float *src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct K2Args {
+    const float *in;
+    long long in_pitch, in_img;
+    float *ll;                             // LL destination (scratch or out)
+    long long ll_pitch, ll_img;
+    float *hl, *lh, *hh;                   // detail subbands (Mallat positions in out)
+    long long out_pitch, out_img;
+    int W, H;
+    int nslabs, tb, nblk, count;
+    long long ntiles;
+    double c0, c1, c2, c3;                 // lifting coefficients (predict, update, predict, update)
+    double sll, sd, shh;                   // output scaling: LL, HL / LH, HH
+};
+
+__device__ __forceinline__ int wssi(int k, int n)
+{
+    // whole-sample symmetric reflection, any k (period 2 (n - 1))
+    if (n == 1) return 0;
+    const int p = 2 * (n - 1);
+    k %= p;
+    if (k < 0) k += p;
+    return k >= n ? p - k : k;
+}
+
+// Raw quad row r (pixel rows 2r, 2r+1, mirrored) of the lane's 2 quads:
+// pixels x = xb .. xb+3 with xb = 2 (m0 - 2) + 4 lane.
+struct RawRow {
+    float e[4], o[4];                       // even row: a0 b0 a1 b1; odd row: c0 d0 c1 d1
+};
+
+template <bool VEC, bool EDGE>
+__device__ __forceinline__ RawRow load_raw_row(const K2Args &a, const float *img, int r, int xb)
+{
+    int y0 = 2 * r, y1 = 2 * r + 1;
+    if (y0 < 0 || y1 >= a.H) {                        // top / bottom rows: mirror
+        y0 = wssi(y0, a.H);
+        y1 = wssi(y1, a.H);
+    }
+    const float *p0 = img + (long long)y0 * a.in_pitch;
+    const float *p1 = img + (long long)y1 * a.in_pitch;
+    RawRow R;
+    if (VEC && !EDGE) {
+        const float4 u = __ldg(reinterpret_cast<const float4 *>(p0 + xb));
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(p1 + xb));
+        R.e[0] = u.x; R.e[1] = u.y; R.e[2] = u.z; R.e[3] = u.w;
+        R.o[0] = v.x; R.o[1] = v.y; R.o[2] = v.z; R.o[3] = v.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int x = EDGE ? wssi(xb + j, a.W) : xb + j;
+            R.e[j] = __ldg(p0 + x);
+            R.o[j] = __ldg(p1 + x);
+        }
+    }
+    return R;
+}
+
+// carried state per quad (see the step comments in the kernel)
+struct Carry2 {
+    double a, c, d, hl1;        // raw a, c, d and predict-1 HL' of row r-1
+    double hh1, lh1f;           // predict-1 HH' and update-1 LH of row r-2
+    double A, hl2;              // update-1 LL and predict-2 HL' of row r-2
+    double hh2, lh2f;           // predict-2 HH' and update-2 LH of row r-3
+};
+
+__device__ __forceinline__ double shr(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }   // lane + 1
+__device__ __forceinline__ double shl(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }     // lane - 1
+
+template <bool VEC, bool EDGE>
+__device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, int n1, int lane)
+{
+    // interior slabs with 16-byte rows: raw rows stream into a per-warp
+    // shared-memory ring by cp.async (DS rows in flight, no registers held);
+    // edge slabs (horizontal mirroring) load through registers
+    constexpr bool ASYNC = VEC && !EDGE;
+    constexpr int D = ASYNC ? DS : DR;
+    const int Wq = (a.W + 1) >> 1, Wh = a.W >> 1, Hh = a.H >> 1;
+    const float *in = a.in + (long long)img * a.in_img;
+    const int xb = 2 * (m0 - 2) + 4 * lane;
+    Carry2 cy[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) cy[i] = Carry2{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const int r_first = n0 - 2, r_last = n1 + 1;
+    RawRow reg[ASYNC ? 1 : D];
+    auto issue = [&](int j, int r) {               // j: compile-time slot
+        if (ASYNC) {
+            int y0 = 2 * r, y1 = 2 * r + 1;
+            if (y0 < 0 || y1 >= a.H) {
+                y0 = wssi(y0, a.H);
+                y1 = wssi(y1, a.H);
+            }
+            cp_async16(wring + (2 * j) * 128 + 4 * lane, in + (long long)y0 * a.in_pitch + xb);
+            cp_async16(wring + (2 * j + 1) * 128 + 4 * lane, in + (long long)y1 * a.in_pitch + xb);
+        } else {
+            reg[ASYNC ? 0 : j] = load_raw_row<VEC, EDGE>(a, in, r, xb);
+        }
+    };
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        if (r_first + j <= r_last) issue(j, r_first + j);
+        if (ASYNC) cp_async_commit();
+    }
+    const int mo = m0 + 2 * (lane - 1);               // first output quad of the lane (lanes 1..30)
+    const bool out_lane = lane >= 1 && lane <= 30;
+    // rows in groups of D so that every ring slot index is a compile-time
+    // constant (a dynamic index would force the prefetched loads to land)
+    for (int rb = r_first; rb <= r_last; rb += D) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        const int r = rb + j;
+        if (r > r_last) break;
+        RawRow R;
+        if (ASYNC) {
+            cp_async_wait<D - 1>();                    // row r's group (the oldest) has landed
+            const float4 u = *reinterpret_cast<const float4 *>(wring + (2 * j) * 128 + 4 * lane);
+            const float4 v = *reinterpret_cast<const float4 *>(wring + (2 * j + 1) * 128 + 4 * lane);
+            R.e[0] = u.x; R.e[1] = u.y; R.e[2] = u.z; R.e[3] = u.w;
+            R.o[0] = v.x; R.o[1] = v.y; R.o[2] = v.z; R.o[3] = v.w;
+        } else {
+            R = reg[ASYNC ? 0 : j];
+        }
+        if (!ASYNC && r + D <= r_last) issue(j, r + D);
+        double av[2], bv[2], cv[2], dv[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            av[i] = R.e[2 * i]; bv[i] = R.e[2 * i + 1];
+            cv[i] = R.o[2 * i]; dv[i] = R.o[2 * i + 1];
+        }
+        // ---- predict 1, row r (same-row part): HL'1 = b + c0 (a + a[m+1])
+        const double a_nb = shr(av[0]);
+        double hl1[2];
+        hl1[0] = fma(a.c0, av[0] + av[1], bv[0]);
+        hl1[1] = fma(a.c0, av[1] + a_nb, bv[1]);
+        // ---- predict 1 completes row r-1: LH'1 = c + c0 (a + a[n+1]),
+        //      HH'1 = d + c0 (c + c[m+1]) + c0 (HL'1 + HL'1[n+1])
+        const double c_nb = shr(cy[0].c);
+        double lh1[2], hh1[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double cr = (i == 0) ? cy[1].c : c_nb;
+            lh1[i] = fma(a.c0, cy[i].a + av[i], cy[i].c);
+            hh1[i] = fma(a.c0, cy[i].hl1 + hl1[i], fma(a.c0, cy[i].c + cr, cy[i].d));
+        }
+        // ---- update 1, row r-1: LH1 = LH'1 + c1 (HH'1 + HH'1[m-1]),
+        //      HL1 = HL'1 + c1 (HH'1 + HH'1[n-1]),
+        //      LL1 = a + c1 (HL'1 + HL'1[m-1]) + c1 (LH1 + LH1[n-1])
+        const double hh1_l = shl(hh1[1]);
+        const double hl1p_l = shl(cy[1].hl1);
+        double A1[2], B1[2], C1[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double hhl = (i == 0) ? hh1_l : hh1[0];
+            const double hll = (i == 0) ? hl1p_l : cy[0].hl1;
+            C1[i] = fma(a.c1, hh1[i] + hhl, lh1[i]);
+            B1[i] = fma(a.c1, hh1[i] + cy[i].hh1, cy[i].hl1);
+            A1[i] = fma(a.c1, C1[i] + cy[i].lh1f, fma(a.c1, cy[i].hl1 + hll, cy[i].a));
+        }
+        // ---- predict 2 on the update-1 output, row r-1 (same-row part):
+        //      HL'2 = HL1 + c2 (LL1 + LL1[m+1])
+        const double A_nb = shr(A1[0]);
+        double hl2[2];
+        hl2[0] = fma(a.c2, A1[0] + A1[1], B1[0]);
+        hl2[1] = fma(a.c2, A1[1] + A_nb, B1[1]);
+        // ---- predict 2 completes row r-2 (carried A, LH1 = lh1f, HH1 = hh1, HL'2):
+        //      LH'2 = LH1 + c2 (LL1 + LL1[n+1]), HH'2 = HH1 + c2 (LH1 + LH1[m+1]) + c2 (HL'2 + HL'2[n+1])
+        const double C_nb = shr(cy[0].lh1f);
+        double lh2[2], hh2[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double cr = (i == 0) ? cy[1].lh1f : C_nb;
+            lh2[i] = fma(a.c2, cy[i].A + A1[i], cy[i].lh1f);
+            hh2[i] = fma(a.c2, cy[i].hl2 + hl2[i], fma(a.c2, cy[i].lh1f + cr, cy[i].hh1));
+        }
+        // ---- update 2, row r-2
+        const double hh2_l = shl(hh2[1]);
+        const double hl2p_l = shl(cy[1].hl2);
+        double A2[2], B2[2], C2[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double hhl = (i == 0) ? hh2_l : hh2[0];
+            const double hll = (i == 0) ? hl2p_l : cy[0].hl2;
+            C2[i] = fma(a.c3, hh2[i] + hhl, lh2[i]);
+            B2[i] = fma(a.c3, hh2[i] + cy[i].hh2, cy[i].hl2);
+            A2[i] = fma(a.c3, C2[i] + cy[i].lh2f, fma(a.c3, cy[i].hl2 + hll, cy[i].A));
+        }
+        // ---- store output row r-2 (scaled)
+        const int n = r - 2;
+        if (n >= n0 && out_lane) {
+            float oLL[2], oHL[2], oLH[2], oHH[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                oLL[i] = (float)(A2[i] * a.sll);
+                oHL[i] = (float)(B2[i] * a.sd);
+                oLH[i] = (float)(C2[i] * a.sd);
+                oHH[i] = (float)(hh2[i] * a.shh);
+            }
+            float *pll = a.ll + (long long)img * a.ll_img + (long long)n * a.ll_pitch + mo;
+            const long long ob = (long long)img * a.out_img + (long long)n * a.out_pitch + mo;
+            float *phl = a.hl + ob, *plh = a.lh + ob, *phh = a.hh + ob;
+            const bool has_odd = n < Hh;
+            if (VEC && !EDGE) {
+                *reinterpret_cast<float2 *>(pll) = make_float2(oLL[0], oLL[1]);
+                __stcs(reinterpret_cast<float2 *>(phl), make_float2(oHL[0], oHL[1]));
+                if (has_odd) {
+                    __stcs(reinterpret_cast<float2 *>(plh), make_float2(oLH[0], oLH[1]));
+                    __stcs(reinterpret_cast<float2 *>(phh), make_float2(oHH[0], oHH[1]));
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int m = mo + i;
+                    if (m < Wq) {
+                        pll[i] = oLL[i];
+                        if (has_odd) __stcs(plh + i, oLH[i]);
+                    }
+                    if (m < Wh) {
+                        __stcs(phl + i, oHL[i]);
+                        if (has_odd) __stcs(phh + i, oHH[i]);
+                    }
+                }
+            }
+        }
+        // ---- carries
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            cy[i].hh2 = hh2[i];
+            cy[i].lh2f = C2[i];
+            cy[i].A = A1[i];
+            cy[i].hl2 = hl2[i];
+            cy[i].hh1 = hh1[i];
+            cy[i].lh1f = C1[i];
+            cy[i].a = av[i];
+            cy[i].c = cv[i];
+            cy[i].d = dv[i];
+            cy[i].hl1 = hl1[i];
+        }
+        if (ASYNC) {
+            // slot j is free again (its row was consumed above)
+            if (r + D <= r_last) issue(j, r + D);
+            cp_async_commit();
+        }
+    }
+    }
+    if (ASYNC) cp_async_wait<0>();
+}
+
+__device__ __forceinline__ void pdl_wait97() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch97() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <bool VEC>
+__global__ void __launch_bounds__(KT, 4) dwt_k2_level_kernel(const __grid_constant__ K2Args a)
+{
+    pdl_launch97();
+    pdl_wait97();
+    extern __shared__ __align__(16) float k2_smem[];
+    const int lane = threadIdx.x & 31;
+    float *wring = k2_smem + (threadIdx.x >> 5) * (DS * 2 * 128);
+    const long long nwarps = (long long)gridDim.x * KW;
+    const int Wq = (a.W + 1) >> 1, Hq = (a.H + 1) >> 1;
+    const long long per_img = (long long)a.nblk * a.nslabs;
+    for (long long t = (long long)blockIdx.x * KW + (threadIdx.x >> 5); t < a.ntiles; t += nwarps) {
+        const int img = int(t / per_img);
+        const int rr = int(t - img * per_img);
+        const int blk = rr / a.nslabs;
+        const int slab = rr - blk * a.nslabs;
+        const int m0 = slab * OUTQ;
+        const int n0 = blk * a.tb, n1 = min(n0 + a.tb, Hq);
+        // pixel columns 2 (m0 - 2) .. 2 (m0 + 62) - 1 must lie inside the image for the unmirrored path
+        const bool edge = (m0 < 2) || (2 * (m0 + 62) > a.W) || (m0 + OUTQ > Wq);
+        if (edge) k2_tile<VEC, true>(a, wring, img, m0, n0, n1, lane);
+        else k2_tile<VEC, false>(a, wring, img, m0, n0, n1, lane);
+    }
+}
+
+int k2_ctas_per_sm()
+{
+    static int per_sm = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int n = 0;
+        if (cudaFuncSetAttribute(dwt_k2_level_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(K2_SMEM)) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(dwt_k2_level_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(K2_SMEM)) !=
+                cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dwt_k2_level_kernel<true>, KT, K2_SMEM) != cudaSuccess || n < 1)
+            n = 1;
+        per_sm = n;
+    });
+    cudaGetLastError();
+    return per_sm;
+}
+
+struct Wavelet2 {
+    double c0, c1, c2, c3, K;
+};
+
+Wavelet2 wavelet_params(int wavelet)
+{
+    if (wavelet == DWT2_WAVELET_CDF97)
+        return Wavelet2{-1.586134342059924, -0.052980118572961, 0.882911075530934, 0.443506852043971,
+                        1.230174104914001};
+    return Wavelet2{-0.5, 0.25, 0.0, 0.0, 1.0};      // DWT2_WAVELET_CDF53_K2
+}
+
+int32_t launch_k2_level(const dwt2_plan *p, K2Args a, cudaStream_t s)
+{
+    const int Wq = (a.W + 1) / 2, Hq = (a.H + 1) / 2;
+    a.nslabs = (Wq + OUTQ - 1) / OUTQ;
+    const long long warps = (long long)p->sms * k2_ctas_per_sm() * KW;
+    const long long slab_rows = (long long)a.count * a.nslabs * Hq;
+    long long tb = slab_rows / (4 * warps);                   // ~4 tiles per resident warp
+    tb = std::max<long long>(16, std::min<long long>(512, tb)); // 4 warm-up rows per tile: >= 16 rows
+    a.tb = int(tb);
+    a.nblk = int((Hq + tb - 1) / tb);
+    a.ntiles = (long long)a.count * a.nblk * a.nslabs;
+    const long long want = (a.ntiles + KW - 1) / KW;
+    const int grid = int(std::max<long long>(1, std::min<long long>(want, warps / KW)));
+    const bool vec = aligned(a.in, 16) && a.in_pitch % 4 == 0 && (a.count == 1 || a.in_img % 4 == 0) &&
+                     aligned(a.ll, 8) && aligned(a.hl, 8) && aligned(a.lh, 8) && aligned(a.hh, 8) &&
+                     a.ll_pitch % 2 == 0 && a.out_pitch % 2 == 0 &&
+                     (a.count == 1 || (a.ll_img % 2 == 0 && a.out_img % 2 == 0));
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(KT);
+    cfg.dynamicSmemBytes = K2_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = vec ? cudaLaunchKernelEx(&cfg, dwt_k2_level_kernel<true>, a)
+                        : cudaLaunchKernelEx(&cfg, dwt_k2_level_kernel<false>, a);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DWT2_ECUDA);
+    }
+    return DWT2_OK;
+}
+
+}  // namespace
+
+namespace dwt2_detail {
+
+// All levels of the K = 2 lifting kernel (plans created with a wavelet other
+// than DWT2_WAVELET_CDF53); buffer roles as run_levels in dwt2.cu.
+int32_t run_levels_k2(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,
+                      long long out_stride, cudaStream_t s)
+{
+    const Wavelet2 wv = wavelet_params(p->wavelet);
+    for (int k = 0; k < p->levels; ++k) {
+        const LevelGeom &g = p->geom[k];
+        K2Args a;
+        memset(&a, 0, sizeof(a));
+        a.W = g.W;
+        a.H = g.H;
+        a.count = count;
+        a.c0 = wv.c0; a.c1 = wv.c1; a.c2 = wv.c2; a.c3 = wv.c3;
+        a.sll = 1.0 / (wv.K * wv.K);
+        a.sd = 1.0;
+        a.shh = wv.K * wv.K;
+        if (k == 0) {
+            a.in = in;
+            a.in_pitch = p->W;
+            a.in_img = in_stride;
+        } else {
+            const int si = (k - 1) % 2;
+            a.in = p->scratch[si];
+            a.in_pitch = p->sc_pitch[si];
+            a.in_img = p->sc_img_stride[si];
+        }
+        a.hl = out + g.Wq;
+        a.lh = out + (long long)g.Hq * p->W;
+        a.hh = a.lh + g.Wq;
+        a.out_pitch = p->W;
+        a.out_img = out_stride;
+        if (k == p->levels - 1) {
+            a.ll = out;
+            a.ll_pitch = p->W;
+            a.ll_img = out_stride;
+        } else {
+            const int si = k % 2;
+            a.ll = p->scratch[si];
+            a.ll_pitch = p->sc_pitch[si];
+            a.ll_img = p->sc_img_stride[si];
+        }
+        int32_t r = launch_k2_level(p, a, s);
+        if (r != DWT2_OK) return r;
+    }
+    return DWT2_OK;
+}
+
+}  // namespace dwt2_detail

@@ -57,6 +57,7 @@ struct InvArgs {
     int W, H;                              // reconstructed size
     int nslabs, nblk, tb, count;
     long long ntiles;
+    const float *ll_lo, *ll_hi, *d_lo, *d_hi;   // allocation ranges of the LL / detail sources (ring loader)
 };
 
 // Raw coefficients of one quad row as one lane sees them: its 2 quads and,
@@ -261,6 +262,173 @@ __global__ void __launch_bounds__(ITHREADS, 2) dwt53_inverse_level_kernel(const 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Ring variant (16-byte aligned planes and pitches): every warp streams its
+// quad rows through a shared-memory ring by cp.async, IDS rows in flight, so
+// the loads of later rows overlap the arithmetic of earlier ones.  A stage
+// holds, per plane, the window of columns [m0 - 4, m0 + 68) (18 x 16 B).
+// ---------------------------------------------------------------------------
+constexpr int IRW = 4;                         // warps per CTA (ring kernel)
+constexpr int IDS = 6;                         // quad rows in flight per warp
+constexpr int IWIN = 72;                       // window floats per plane
+constexpr int ISTAGE = 4 * IWIN;               // floats per stage
+constexpr size_t IRING_SMEM = size_t(IRW) * IDS * ISTAGE * sizeof(float);
+
+__device__ __forceinline__ void icp_async16(float *dst, const float *src, uint32_t nbytes)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                 ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(src), "r"(nbytes) : "memory");
+}
+__device__ __forceinline__ void icp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void icp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// issue the 72 chunks of quad row n (4 planes x 18) into stage `st`
+__device__ __forceinline__ void ring_issue(const InvArgs &a, float *st, int img, int n, int m0, int lane)
+{
+    const int Hh = a.H >> 1;
+    const int nd = min(max(n, 0), Hh - 1);
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        const int c = lane + 32 * t;
+        if (c < 72) {
+            const int pl = c / 18, k = c - pl * 18;
+            const float *base = pl == 0 ? a.ll : pl == 1 ? a.hl : pl == 2 ? a.lh : a.hh;
+            const long long row = (pl == 0 || pl == 1) ? n : nd;
+            const long long pitch = pl == 0 ? a.ll_pitch : a.d_pitch;
+            const long long img_off = (long long)img * (pl == 0 ? a.ll_img : a.d_img);
+            const float *src = base + img_off + row * pitch + (m0 - 4 + 4 * k);
+            const float *lo = pl == 0 ? a.ll_lo : a.d_lo, *hi = pl == 0 ? a.ll_hi : a.d_hi;
+            uint32_t nb = (src >= lo && src + 4 <= hi) ? 16u : 0u;    // outside the allocation: zero fill
+            icp_async16(st + pl * IWIN + 4 * k, nb ? src : lo, nb);
+        }
+    }
+}
+
+template <bool EDGE>
+__device__ __forceinline__ Raw ring_read(const InvArgs &a, const float *st, int m0, int lane)
+{
+    const int Wq = (a.W + 1) >> 1, Wh = a.W >> 1;
+    const int o = m0 - 4;                        // window column 0
+    const int m = m0 + 2 * lane;
+    Raw r;
+    if (!EDGE) {
+        const float2 ll = *reinterpret_cast<const float2 *>(st + 0 * IWIN + (m - o));
+        const float2 hl = *reinterpret_cast<const float2 *>(st + 1 * IWIN + (m - o));
+        const float2 lh = *reinterpret_cast<const float2 *>(st + 2 * IWIN + (m - o));
+        const float2 hh = *reinterpret_cast<const float2 *>(st + 3 * IWIN + (m - o));
+        r.LL[0] = ll.x; r.LL[1] = ll.y; r.HL[0] = hl.x; r.HL[1] = hl.y;
+        r.LH[0] = lh.x; r.LH[1] = lh.y; r.HH[0] = hh.x; r.HH[1] = hh.y;
+        r.hlL = st[1 * IWIN + (m0 - 1 - o)];
+        r.hhL = st[3 * IWIN + (m0 - 1 - o)];
+        r.llR = st[0 * IWIN + (m0 + IQ - o)];
+        r.hlR = st[1 * IWIN + (m0 + IQ - o)];
+        r.lhR = st[2 * IWIN + (m0 + IQ - o)];
+        r.hhR = st[3 * IWIN + (m0 + IQ - o)];
+    } else {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int mL = min(m + i, Wq - 1) - o, mH = min(max(m + i, 0), Wh - 1) - o;
+            r.LL[i] = st[0 * IWIN + mL];
+            r.LH[i] = st[2 * IWIN + mL];
+            r.HL[i] = st[1 * IWIN + mH];
+            r.HH[i] = st[3 * IWIN + mH];
+        }
+        const int mh = max(m0 - 1, 0) - o;
+        r.hlL = st[1 * IWIN + mh];
+        r.hhL = st[3 * IWIN + mh];
+        const int mrL = min(m0 + IQ, Wq - 1) - o, mrH = min(m0 + IQ, Wh - 1) - o;
+        r.llR = st[0 * IWIN + mrL];
+        r.lhR = st[2 * IWIN + mrL];
+        r.hlR = st[1 * IWIN + mrH];
+        r.hhR = st[3 * IWIN + mrH];
+    }
+    return r;
+}
+
+template <bool EDGE>
+__device__ __forceinline__ void ring_tile(const InvArgs &a, float *ring, int img, int m0, int n0, int n1, int lane)
+{
+    const int Hq = (a.H + 1) >> 1;
+    // load sequence: i = 0 -> row max(n0-1, 0) (seeds the n-1 carry), i >= 1 -> row n0 + i - 1
+    const int T = 1 + (min(n1, Hq - 1) - n0 + 1);
+    auto row_of = [&](int i) { return i == 0 ? max(n0 - 1, 0) : n0 + i - 1; };
+#pragma unroll
+    for (int j = 0; j < IDS; ++j) {
+        if (j < T) ring_issue(a, ring + j * ISTAGE, img, row_of(j), m0, lane);
+        icp_commit();
+    }
+    Rec prev;
+    for (int ib = 0; ib < T; ib += IDS) {
+#pragma unroll
+        for (int j = 0; j < IDS; ++j) {
+            const int i = ib + j;
+            if (i >= T) break;
+            icp_wait<IDS - 1>();
+            const Raw raw = ring_read<EDGE>(a, ring + j * ISTAGE, m0, lane);
+            if (i == 0) {
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    prev.hh[q] = raw.HH[q];
+                    prev.lh[q] = raw.LH[q];
+                }
+                prev.hhL = raw.hhL;
+                prev.hhR = raw.hhR;
+                prev.lhR = raw.lhR;
+            } else {
+                const int n = n0 + i - 1;
+                const Rec rc = undo_update(raw, prev, lane);
+                if (n > n0) undo_predict_store<true, EDGE>(a, prev, rc, img, n - 1, m0, lane, true);
+                prev = rc;
+            }
+            // the stage's values are in registers (used above): refill it
+            if (i + IDS < T) ring_issue(a, ring + j * ISTAGE, img, row_of(i + IDS), m0, lane);
+            icp_commit();
+        }
+    }
+    icp_wait<0>();
+    if (n1 == Hq) undo_predict_store<true, EDGE>(a, prev, prev, img, n1 - 1, m0, lane, (a.H & 1) == 0);
+}
+
+__global__ void __launch_bounds__(IRW * 32, 3) dwt53_inverse_ring_kernel(const __grid_constant__ InvArgs a)
+{
+    extern __shared__ __align__(16) float iring_smem[];
+    pdl_launch_inv();
+    pdl_wait_inv();
+    const int lane = threadIdx.x & 31;
+    float *ring = iring_smem + (threadIdx.x >> 5) * (IDS * ISTAGE);
+    const long long nwarps = (long long)gridDim.x * IRW;
+    const int Wq = (a.W + 1) >> 1, Hq = (a.H + 1) >> 1;
+    const long long per_img = (long long)a.nblk * a.nslabs;
+    for (long long t = (long long)blockIdx.x * IRW + (threadIdx.x >> 5); t < a.ntiles; t += nwarps) {
+        const int img = int(t / per_img);
+        const int r = int(t - (long long)img * per_img);
+        const int blk = r / a.nslabs;
+        const int slab = r - blk * a.nslabs;
+        const int m0 = slab * IQ;
+        const int n0 = blk * a.tb, n1 = min(n0 + a.tb, Hq);
+        if ((m0 == 0) || (m0 + IQ >= Wq)) ring_tile<true>(a, ring, img, m0, n0, n1, lane);
+        else ring_tile<false>(a, ring, img, m0, n0, n1, lane);
+    }
+}
+
+int inverse_ring_ctas_per_sm()
+{
+    static int per_sm = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int n = 0;
+        if (cudaFuncSetAttribute(dwt53_inverse_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(IRING_SMEM)) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dwt53_inverse_ring_kernel, IRW * 32, IRING_SMEM) !=
+                cudaSuccess || n < 1)
+            n = 1;
+        per_sm = n;
+    });
+    cudaGetLastError();
+    return per_sm;
+}
+
 int inverse_ctas_per_sm()
 {
     static int per_sm = 0;
@@ -281,6 +449,38 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
     InvArgs a = base;
     const int Wq = (a.W + 1) / 2, Hq = (a.H + 1) / 2;
     a.nslabs = (Wq + IQ - 1) / IQ;
+    // ring kernel: every plane row 16-byte aligned (cp.async chunks), float4 stores
+    const bool ring = aligned(a.ll, 16) && aligned(a.hl, 16) && aligned(a.lh, 16) && aligned(a.hh, 16) &&
+                      a.ll_pitch % 4 == 0 && a.d_pitch % 4 == 0 &&
+                      (a.count == 1 || (a.ll_img % 4 == 0 && a.d_img % 4 == 0)) &&
+                      aligned(a.out, 16) && a.out_pitch % 4 == 0 && (a.count == 1 || a.out_img % 4 == 0);
+    if (ring) {
+        const long long rwarps = (long long)p->sms * inverse_ring_ctas_per_sm() * IRW;
+        const long long slab_rows = (long long)a.count * a.nslabs * Hq;
+        long long tb = slab_rows / (8 * rwarps);
+        tb = std::max<long long>(8, std::min<long long>(256, tb));
+        a.tb = int(tb);
+        a.nblk = int((Hq + tb - 1) / tb);
+        a.ntiles = (long long)a.count * a.nblk * a.nslabs;
+        const long long want = (a.ntiles + IRW - 1) / IRW;
+        const int grid = int(std::max<long long>(1, std::min<long long>(want, rwarps / IRW)));
+        cudaLaunchConfig_t cfg;
+        memset(&cfg, 0, sizeof(cfg));
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(IRW * 32);
+        cfg.dynamicSmemBytes = IRING_SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, dwt53_inverse_ring_kernel, a) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(DWT2_ECUDA);
+        }
+        return DWT2_OK;
+    }
     const long long warps = (long long)p->sms * inverse_ctas_per_sm() * IWARPS;
     // tile height: ~8 tiles per resident warp, at least 8 quad rows (the
     // halo row re-read costs 1 / tb), at most 256
@@ -352,6 +552,16 @@ int32_t run_inverse(const dwt2_plan *p, const float *in, float *out, int count, 
             a.out_pitch = p->sc_pitch[sidx];
             a.out_img = p->sc_img_stride[sidx];
         }
+        a.d_lo = in;
+        a.d_hi = in + (long long)(count - 1) * in_stride + (long long)p->W * p->H;
+        if (k == p->levels - 1) {
+            a.ll_lo = a.d_lo;
+            a.ll_hi = a.d_hi;
+        } else {
+            const int sidx = k % 2;
+            a.ll_lo = p->scratch[sidx];
+            a.ll_hi = p->scratch[sidx] + (long long)count * p->sc_img_stride[sidx];
+        }
         int32_t r = launch_inverse_level(p, a, s);
         if (r != DWT2_OK) return r;
     }
@@ -365,6 +575,7 @@ extern "C" {
 int32_t dwt2_inverse(const dwt2_plan *p, const float *in, float *out, dwt2_stream_t stream)
 {
     if (!p || !in || !out || p->strip || !aligned(in, 4) || !aligned(out, 4)) return fail(DWT2_EINVAL);
+    if (p->wavelet != DWT2_WAVELET_CDF53) return fail(DWT2_EUNSUPPORTED);
     const size_t bytes = size_t(p->W) * p->H * sizeof(float);
     if (overlap(in, bytes, out, bytes) || !on_plan_device(p, in) || !on_plan_device(p, out))
         return fail(DWT2_EINVAL);
@@ -382,6 +593,7 @@ int32_t dwt2_inverse_batched(const dwt2_plan *p, const float *in, float *out, in
     if (!p || !in || !out || p->strip || count < 1 || count > p->max_count || in_stride < img ||
         out_stride < img || !aligned(in, 4) || !aligned(out, 4))
         return fail(DWT2_EINVAL);
+    if (p->wavelet != DWT2_WAVELET_CDF53) return fail(DWT2_EUNSUPPORTED);
     const size_t in_bytes = size_t((count - 1) * in_stride + img) * sizeof(float);
     const size_t out_bytes = size_t((count - 1) * out_stride + img) * sizeof(float);
     if (overlap(in, in_bytes, out, out_bytes) || !on_plan_device(p, in) || !on_plan_device(p, out))

@@ -401,6 +401,7 @@ int32_t dwt2_scheme_steps(int32_t scheme)
 int32_t dwt2_forward_scheme(const dwt2_plan *p, int32_t scheme, const float *in, float *out, int32_t count,
                             int64_t in_stride, int64_t out_stride, dwt2_stream_t stream)
 {
+    if (p && p->wavelet != DWT2_WAVELET_CDF53) return fail(DWT2_EUNSUPPORTED);
     if (scheme == DWT2_SCHEME_FUSED) return dwt2_forward_batched(p, in, out, count, in_stride, out_stride, stream);
     const long long img = (long long)(p ? p->W : 0) * (p ? p->H : 0);
     if (!p || !in || !out || p->strip || count < 1 || count > p->max_count || in_stride < img ||

@@ -1,7 +1,8 @@
 """The paper's scheme comparison (section 4, Fig. 6) on
 B200: every scheme of csrc/schemes.cu plus the fused product kernel, one
 level of the forward 2-D CDF 5/3 DWT on integer-valued images of edge
-1024 .. 16384 (inputs in HBM, L2 flushed before every timed iteration).
+1024 .. 16384 (protocol of scripts/_timing.py: K calls in one CUDA graph,
+distinct input/output pairs for small sizes, L2 flushed before the replay).
 
 A step boundary is a kernel boundary, so the schemes differ in HBM round
 trips: algorithmic bytes per pixel = 8 (1 step, fused / naive), 16 (2 steps:
@@ -25,6 +26,8 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_1708_07853_b200 import dwt2, workloads  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _timing import n_pairs, time_calls  # noqa: E402
 
 BYTES = {"fused": 8, "nonsep_naive": 8, "nonsep_lifting": 16, "nonsep_adapted": 16, "sep_conv": 16,
          "sep_lifting": 26}
@@ -36,12 +39,10 @@ PAPER = {"fused": "Eq. 5 fused (product)", "nonsep_naive": "Eq. 5, 1 plain kerne
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default="1024,2048,4096,8192,16384")
-    ap.add_argument("--iters", type=int, default=30)
+    ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "scheme_compare.json"))
     args = ap.parse_args()
     torch.cuda.set_device(0)
-    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > L2
-    sink = torch.zeros((), device="cuda")
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     rows = []
@@ -50,47 +51,23 @@ def main():
         plan = dwt2.Plan(edge, edge, 1)
         ref = plan.forward(x)
         torch.cuda.synchronize()
+        npairs = n_pairs(8 * edge * edge, args.iters)
+        pairs = [(x if i == 0 else x.clone(), torch.empty_like(x)) for i in range(npairs)]
         for scheme in BYTES:
             out = torch.empty_like(x)
             plan.forward_scheme(scheme, x, out)
             torch.cuda.synchronize()
             exact = bool(torch.equal(out, ref))
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                plan.forward_scheme(scheme, x, out)
-            fg = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(fg):
-                sink.copy_(flush.amax())          # read-only: evicts L2 with clean lines
-            for _ in range(3):
-                fg.replay()
-                g.replay()
-            torch.cuda.synchronize()
-            # K (flush + call) back to back minus K flushes alone: CUDA event
-            # timestamps tick every 2.048 us here (scripts/diag_small.py)
-            ts = []
-            for _ in range(5):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                for _ in range(args.iters):
-                    fg.replay()
-                    g.replay()
-                e1.record()
-                f0.record()
-                for _ in range(args.iters):
-                    fg.replay()
-                f1.record()
-                torch.cuda.synchronize()
-                ts.append((e0.elapsed_time(e1) - f0.elapsed_time(f1)) * 1e3 / args.iters)
-            us = statistics.median(ts)
+            us = time_calls(lambda p, s=scheme: plan.forward_scheme(s, p[0], p[1]), pairs, args.iters)
             px = edge * edge
             r = {"edge": edge, "scheme": scheme, "paper": PAPER[scheme],
-                 "steps": dwt2.dwt2_scheme_steps(dwt2.SCHEMES[scheme]), "us_median": us, "us_min": min(ts),
+                 "steps": dwt2.dwt2_scheme_steps(dwt2.SCHEMES[scheme]), "us": us,
                  "gpix_s": px / us / 1e3, "ns_per_pel": us * 1e3 / px,
                  "algo_bytes_per_px": BYTES[scheme], "algo_gbs": BYTES[scheme] * px / us / 1e3,
                  "frac_of_copy": BYTES[scheme] * px / us / 1e3 / peak, "bit_exact_vs_fused": exact}
             rows.append(r)
             print(json.dumps(r), flush=True)
+        del pairs
         plan.close()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
@@ -102,7 +79,7 @@ def main():
         cells = []
         for s in BYTES:
             r = next(r for r in rows if r["edge"] == edge and r["scheme"] == s)
-            cells.append(f"{r['us_median']:.1f} us ({r['frac_of_copy']:.2f})")
+            cells.append(f"{r['us']:.1f} us ({r['frac_of_copy']:.2f})")
         print(f"| {edge} | " + " | ".join(cells) + " |")
 
 

@@ -127,3 +127,18 @@ def test_inverse_rejects_strip_and_overlap():
     with pytest.raises(dwt2.DWT2Error):
         dwt2.dwt2_inverse(sp._p, buf.data_ptr(), out.data_ptr(), 0)
     sp.close()
+
+
+@pytest.mark.parametrize("W,H,L,N", [(512, 264, 3, 3), (1024, 40, 2, 2), (256, 1000, 4, 4)])
+def test_inverse_batched_ring_path(W, H, L, N):
+    """Widths with 16-byte aligned subband planes take the cp.async ring
+    kernel (levels whose planes stay aligned); batched pyramids against the
+    oracle, image by image."""
+    xs = np.stack([workloads.uniform_real(W, H, 70 + i) for i in range(N)])
+    ys = np.stack([coeffs_of(x, L) for x in xs])
+    plan = dwt2.Plan(W, H, L, max_count=N)
+    got = plan.inverse(torch.from_numpy(ys).cuda()).cpu().numpy()
+    plan.close()
+    for i in range(N):
+        y64 = ys[i].astype(np.float64)
+        compare(got[i], oracle.inverse(y64, L), oracle.inverse(y64, L, round_f32=True), False, f"ring batch {i}")
