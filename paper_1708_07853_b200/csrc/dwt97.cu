@@ -154,20 +154,26 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
             reg[ASYNC ? 0 : j] = load_raw_row<VEC, EDGE>(a, in, r, xb);
         }
     };
+    // the row loop runs in whole groups of D rows (rows past r_last are
+    // mirrored reads whose outputs are not stored): no early exit, so the
+    // shuffles stay in provably convergent code
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        if (r_first + j <= r_last) issue(j, r_first + j);
+        issue(j, r_first + j);
         if (ASYNC) cp_async_commit();
     }
     const int mo = m0 + 2 * (lane - 1);               // first output quad of the lane (lanes 1..30)
     const bool out_lane = lane >= 1 && lane <= 30;
+    // output cursors at row r - 2 of the walk, advanced one row per iteration
+    float *cll = a.ll + (long long)img * a.ll_img + (long long)(r_first - 2) * a.ll_pitch + mo;
+    const long long ob0 = (long long)img * a.out_img + (long long)(r_first - 2) * a.out_pitch + mo;
+    float *chl = a.hl + ob0, *clh = a.lh + ob0, *chh = a.hh + ob0;
     // rows in groups of D so that every ring slot index is a compile-time
     // constant (a dynamic index would force the prefetched loads to land)
     for (int rb = r_first; rb <= r_last; rb += D) {
 #pragma unroll
     for (int j = 0; j < D; ++j) {
         const int r = rb + j;
-        if (r > r_last) break;
         RawRow R;
         if (ASYNC) {
             cp_async_wait<D - 1>();                    // row r's group (the oldest) has landed
@@ -178,7 +184,7 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
         } else {
             R = reg[ASYNC ? 0 : j];
         }
-        if (!ASYNC && r + D <= r_last) issue(j, r + D);
+        if (!ASYNC) issue(j, r + D);
         double av[2], bv[2], cv[2], dv[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
@@ -244,7 +250,7 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
         }
         // ---- store output row r-2 (scaled)
         const int n = r - 2;
-        if (n >= n0 && out_lane) {
+        if (n >= n0 && n < n1 && out_lane) {
             float oLL[2], oHL[2], oLH[2], oHH[2];
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
@@ -253,9 +259,7 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
                 oLH[i] = (float)(C2[i] * a.sd);
                 oHH[i] = (float)(hh2[i] * a.shh);
             }
-            float *pll = a.ll + (long long)img * a.ll_img + (long long)n * a.ll_pitch + mo;
-            const long long ob = (long long)img * a.out_img + (long long)n * a.out_pitch + mo;
-            float *phl = a.hl + ob, *plh = a.lh + ob, *phh = a.hh + ob;
+            float *pll = cll, *phl = chl, *plh = clh, *phh = chh;
             const bool has_odd = n < Hh;
             if (VEC && !EDGE) {
                 *reinterpret_cast<float2 *>(pll) = make_float2(oLL[0], oLL[1]);
@@ -279,6 +283,10 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
                 }
             }
         }
+        cll += a.ll_pitch;
+        chl += a.out_pitch;
+        clh += a.out_pitch;
+        chh += a.out_pitch;
         // ---- carries
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
@@ -295,7 +303,7 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
         }
         if (ASYNC) {
             // slot j is free again (its row was consumed above)
-            if (r + D <= r_last) issue(j, r + D);
+            if (rb + D <= r_last) issue(j, r + D);       // the next group exists
             cp_async_commit();
         }
     }

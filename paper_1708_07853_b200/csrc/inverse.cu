@@ -283,24 +283,47 @@ __device__ __forceinline__ void icp_commit() { asm volatile("cp.async.commit_gro
 template <int N>
 __device__ __forceinline__ void icp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// issue the 72 chunks of quad row n (4 planes x 18) into stage `st`
-__device__ __forceinline__ void ring_issue(const InvArgs &a, float *st, int img, int n, int m0, int lane)
+// Per-lane share of a stage: chunks c = lane, lane + 32, lane + 64 (< 72) of
+// the 4 x 18 16-byte chunks; fixed for the whole kernel, so the plane
+// selection is done once per tile (ChunkPlan) and a row costs one address
+// update per chunk.
+struct ChunkPlan {
+    const float *src[3];        // chunk address at row 0 (image and column applied)
+    long long pitch[3];
+    int dst[3];                 // float offset in the stage
+    bool lh_hh[3];              // rows clamped to the LH / HH range
+    const float *lo[3], *hi[3]; // allocation range (zero fill outside)
+};
+
+__device__ __forceinline__ ChunkPlan chunk_plan(const InvArgs &a, int img, int m0, int lane)
 {
-    const int Hh = a.H >> 1;
-    const int nd = min(max(n, 0), Hh - 1);
+    ChunkPlan P;
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
-        const int c = lane + 32 * t;
-        if (c < 72) {
-            const int pl = c / 18, k = c - pl * 18;
-            const float *base = pl == 0 ? a.ll : pl == 1 ? a.hl : pl == 2 ? a.lh : a.hh;
-            const long long row = (pl == 0 || pl == 1) ? n : nd;
-            const long long pitch = pl == 0 ? a.ll_pitch : a.d_pitch;
-            const long long img_off = (long long)img * (pl == 0 ? a.ll_img : a.d_img);
-            const float *src = base + img_off + row * pitch + (m0 - 4 + 4 * k);
-            const float *lo = pl == 0 ? a.ll_lo : a.d_lo, *hi = pl == 0 ? a.ll_hi : a.d_hi;
-            uint32_t nb = (src >= lo && src + 4 <= hi) ? 16u : 0u;    // outside the allocation: zero fill
-            icp_async16(st + pl * IWIN + 4 * k, nb ? src : lo, nb);
+        const int c = min(lane + 32 * t, 71);
+        const int pl = c / 18, k = c - pl * 18;
+        const float *base = pl == 0 ? a.ll : pl == 1 ? a.hl : pl == 2 ? a.lh : a.hh;
+        const long long img_off = (long long)img * (pl == 0 ? a.ll_img : a.d_img);
+        P.src[t] = base + img_off + (m0 - 4 + 4 * k);
+        P.pitch[t] = pl == 0 ? a.ll_pitch : a.d_pitch;
+        P.dst[t] = pl * IWIN + 4 * k;
+        P.lh_hh[t] = pl >= 2;
+        P.lo[t] = pl == 0 ? a.ll_lo : a.d_lo;
+        P.hi[t] = pl == 0 ? a.ll_hi : a.d_hi;
+    }
+    return P;
+}
+
+// issue the 72 chunks of quad row n (4 planes x 18) into stage `st`
+__device__ __forceinline__ void ring_issue(const InvArgs &a, const ChunkPlan &P, float *st, int n, int lane)
+{
+    const int nd = min(max(n, 0), (a.H >> 1) - 1);
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        if (t < 2 || lane < 8) {
+            const float *src = P.src[t] + (long long)(P.lh_hh[t] ? nd : n) * P.pitch[t];
+            const uint32_t nb = (src >= P.lo[t] && src + 4 <= P.hi[t]) ? 16u : 0u;   // outside: zero fill
+            icp_async16(st + P.dst[t], nb ? src : P.lo[t], nb);
         }
     }
 }
@@ -350,12 +373,13 @@ template <bool EDGE>
 __device__ __forceinline__ void ring_tile(const InvArgs &a, float *ring, int img, int m0, int n0, int n1, int lane)
 {
     const int Hq = (a.H + 1) >> 1;
+    const ChunkPlan P = chunk_plan(a, img, m0, lane);
     // load sequence: i = 0 -> row max(n0-1, 0) (seeds the n-1 carry), i >= 1 -> row n0 + i - 1
     const int T = 1 + (min(n1, Hq - 1) - n0 + 1);
     auto row_of = [&](int i) { return i == 0 ? max(n0 - 1, 0) : n0 + i - 1; };
 #pragma unroll
     for (int j = 0; j < IDS; ++j) {
-        if (j < T) ring_issue(a, ring + j * ISTAGE, img, row_of(j), m0, lane);
+        if (j < T) ring_issue(a, P, ring + j * ISTAGE, row_of(j), lane);
         icp_commit();
     }
     Rec prev;
@@ -382,7 +406,7 @@ __device__ __forceinline__ void ring_tile(const InvArgs &a, float *ring, int img
                 prev = rc;
             }
             // the stage's values are in registers (used above): refill it
-            if (i + IDS < T) ring_issue(a, ring + j * ISTAGE, img, row_of(i + IDS), m0, lane);
+            if (i + IDS < T) ring_issue(a, P, ring + j * ISTAGE, row_of(i + IDS), lane);
             icp_commit();
         }
     }
