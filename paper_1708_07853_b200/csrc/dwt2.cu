@@ -216,6 +216,13 @@ __device__ __forceinline__ void cp_async_16(float *dst, const void *src, uint32_
                  ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes) : "memory");
 }
 
+// 1-D bulk copy global -> shared (16-byte granules), completing on an mbarrier
+__device__ __forceinline__ void bulk_copy_g2s(float *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar)
 {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -533,7 +540,7 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + size_t(WARPS) * Ring<TMA>::FLOATS * sizeof(float)) + warp * S;
 
     if (lane == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], TMA ? 1u : 32u);
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1u);     // one arrive.expect_tx per stage
         fence_mbar_init();
     }
     __syncwarp();
@@ -609,31 +616,61 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
                     tma_load_3d(dst + Lay<TMA>::SUB, &a.tmap, pt.x0 + BOX1, r0 - a.in_row0, pt.img, &bars[slot]);
             }
         } else {
-            // per box and row: 35 aligned 16-byte chunks cover [start - delta, start + 140 - delta)
+            // Unaligned rows (odd widths, e.g. config 5's 4095-wide images):
+            // one 1-D bulk copy per box row (cp.async.bulk, 16-byte granules)
+            // of the 140 floats from the row's 16-byte-aligned address at or
+            // below column x0 + BOX0 (the consumer re-derives the shift).  Lane
+            // i < NBOX * BOXH copies row i.  Clamped to [in, in_end): the first
+            // bytes of the buffer start at `in` (4 floats later in smem; the
+            // skipped columns lie left of the image and are never read), and
+            // the last < 16 bytes of the buffer are copied by lane 0 with plain
+            // loads before its arrive.  Rows outside the buffer are not copied.
             const float *img_in = a.in + (long long)pt.img * a.in_img_stride;
-            constexpr int CPR = Lay<false>::RP / 4;
-            for (int idx = lane; idx < NBOX * BOXH * CPR; idx += 32) {
-                const int bx = idx / (BOXH * CPR);
-                const int rem = idx - bx * (BOXH * CPR);
-                const int rr = rem / CPR;
-                const int c = rem - rr * CPR;
+            const uintptr_t lo = reinterpret_cast<uintptr_t>(a.in);
+            const uintptr_t hi = reinterpret_cast<uintptr_t>(a.in_end);
+            const uintptr_t hi16 = hi & ~uintptr_t(15);
+            uint32_t my_bytes = 0;
+            uintptr_t my_src = 0;
+            float *my_dst = nullptr;
+            if (lane < NBOX * BOXH) {
+                const int bx = lane / BOXH, rr = lane - bx * BOXH;
                 const int br = r0 + rr - a.in_row0;
-                uint32_t nbytes = 0;     // 0: zero-fill, no global access
-                const char *src = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(a.in) & ~uintptr_t(15));
                 if (br >= 0 && br < a.in_rows) {
                     const float *rowp = img_in + (long long)br * a.in_pitch + (pt.x0 + (bx ? BOX1 : BOX0));
-                    const uintptr_t al = reinterpret_cast<uintptr_t>(rowp) & ~uintptr_t(15);
-                    const uintptr_t ch = al + uintptr_t(16) * c;
-                    const uintptr_t lo = reinterpret_cast<uintptr_t>(a.in);
-                    const uintptr_t hi = reinterpret_cast<uintptr_t>(a.in_end);
-                    if (ch < hi && ch + 16 > lo) {
-                        nbytes = uint32_t((hi - ch) < 16 ? (hi - ch) : 16);
-                        src = reinterpret_cast<const char *>(ch);
+                    uintptr_t st = reinterpret_cast<uintptr_t>(rowp) & ~uintptr_t(15);
+                    uintptr_t en = st + 4 * Lay<false>::RP;
+                    float *d = dst + bx * Lay<false>::SUB + rr * Lay<false>::RP;
+                    if (st < lo) {                  // left of the buffer start
+                        d += (lo - st) / 4;
+                        st = lo;
+                    }
+                    if (en > hi16) en = hi16;       // the < 16-byte tail: lane 0 below
+                    if (en > st) {
+                        my_bytes = uint32_t(en - st);
+                        my_src = st;
+                        my_dst = d;
+                    }
+                    if (hi > hi16 && reinterpret_cast<uintptr_t>(rowp) + 4 * Lay<false>::RP > hi16 &&
+                        reinterpret_cast<uintptr_t>(rowp) < hi) {
+                        // this row reaches into the unaligned tail of the buffer
+                        const uintptr_t st0 = reinterpret_cast<uintptr_t>(rowp) & ~uintptr_t(15);
+                        float *dt = dst + bx * Lay<false>::SUB + rr * Lay<false>::RP + (hi16 - st0) / 4;
+                        const float *tail = reinterpret_cast<const float *>(hi16);
+                        const uintptr_t room = Lay<false>::RP - (hi16 - st0) / 4;    // stay inside the smem row
+                        const uintptr_t nt = (hi - hi16) / 4 < room ? (hi - hi16) / 4 : room;
+                        for (uintptr_t k = 0; k < nt; ++k) dt[k] = tail[k];
                     }
                 }
-                cp_async_16(dst + bx * Lay<false>::SUB + rr * Lay<false>::RP + 4 * c, src, nbytes);
             }
-            cp_async_mbar_arrive(&bars[slot]);
+            // total bytes of the stage (warp sum), posted by lane 0 with its arrival
+            uint32_t total = my_bytes;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+            // plain smem stores of the tail must be visible to the async proxy / consumers
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(&bars[slot], total);
+            if (my_bytes) bulk_copy_g2s(my_dst, reinterpret_cast<const void *>(my_src), my_bytes, &bars[slot]);
         }
         ++pt_j;
         ++prod_seq;
