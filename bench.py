@@ -419,6 +419,7 @@ def main():
     device = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
+        dist.barrier()          # communicator up before the first grouped send/recv (all ranks)
 
     OursRunner.overlap_off = args.no_overlap
     OursRunner.steps = args.steps

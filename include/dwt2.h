@@ -74,7 +74,8 @@ enum {
     DWT2_WAVELET_CDF97 = 1,    /* CDF 9/7: Eq. (5) for K = 2 lifting pairs + scaling, one fused kernel per
                                   level; constants of Daubechies & Sweldens, JPEG 2000 normalisation
                                   (low / K, high * K; DESIGN.md C-B1..C-B3) */
-    DWT2_WAVELET_CDF53_K2 = 2  /* CDF 5/3 through the K = 2 kernel (second pair = 0, K = 1): a cross-check */
+    DWT2_WAVELET_CDF53_K2 = 2, /* CDF 5/3 through the K = 2 kernel (second pair = 0, K = 1): a cross-check */
+    DWT2_WAVELET_LIFTING = 3   /* any wavelet of <= 2 symmetric lifting pairs (dwt2_plan_create_lifting) */
 };
 
 enum {                         /* dwt2_forward_strip `part` */
@@ -96,6 +97,18 @@ dwt2_plan *dwt2_plan_create(int32_t width, int32_t height, int32_t levels, int32
  * fp64 definition within fp32 rounding of each level's output. */
 dwt2_plan *dwt2_plan_create_ex(int32_t width, int32_t height, int32_t levels, int32_t boundary, int32_t wavelet,
                                int32_t max_count);
+
+/* Plan for a general lifting wavelet (SURVEY.md 8f N4 "general lifting
+ * wavelets"): at most two predict / update pairs of the symmetric 2-tap form
+ * of Eq. (2) and a scaling,
+ *     predict k:  d[i] += p_k (s[i] + s[i+1])      (P = p_k (1 + z))
+ *     update  k:  s[i] += u_k (d[i-1] + d[i])      (U = u_k (1 + z^-1))
+ *     scaling:    low = s / K, high = d * K,
+ * coeffs = {p1, u1, p2, u2} (host array, copied), K > 0 and finite; unused
+ * pairs are 0.  Evaluated by the non-separable K = 2 kernel (dwt97.cu) as
+ * DWT2_WAVELET_LIFTING; supports what DWT2_WAVELET_CDF97 plans support. */
+dwt2_plan *dwt2_plan_create_lifting(int32_t width, int32_t height, int32_t levels, int32_t boundary,
+                                    const double *coeffs, double K, int32_t max_count);
 
 /* As dwt2_plan_create, with scratch for up to max_count images per
  * dwt2_forward_batched call (BASELINE.json config 5). */

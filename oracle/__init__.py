@@ -63,6 +63,8 @@ def _load():
         lib.oracle_dwt97_forward.restype = L
         lib.oracle_dwt97_inverse.argtypes = [dp, dp, L, L, L, ctypes.c_int]
         lib.oracle_dwt97_inverse.restype = L
+        lib.oracle_lift2_forward.argtypes = [dp, dp, L, L, L, ctypes.c_int, dp, ctypes.c_double]
+        lib.oracle_lift2_forward.restype = L
         lib.oracle_dwt97_conv_sample_f32.argtypes = [fp, L, L, L, L, ip, lp, lp, dp]
         lib.oracle_wss_index.argtypes = [L, L]
         lib.oracle_wss_index.restype = L
@@ -123,6 +125,21 @@ def forward(img, levels: int = 1, round_f32: bool = False, algorithm: str = "lif
         fn = _load().oracle_dwt53_fwd_lifting if algorithm == "lifting" else _load().oracle_dwt53_fwd_conv
         r = fn(_dptr(img), _dptr(out), W, H, levels, int(bool(round_f32)))
     if r < 0:
+        raise ValueError("oracle: invalid arguments")
+    return out
+
+
+def forward_lifting2(img, levels: int, coeffs, K: float, round_f32: bool = False) -> np.ndarray:
+    """General K <= 2 lifting wavelet: coeffs = (p1, u1, p2, u2), scaling K
+    (low / K, high * K).  (-1/2, 1/4, 0, 0), 1 is CDF 5/3; the 9/7 constants
+    give CDF 9/7 (both pinned in the tests)."""
+    img = np.ascontiguousarray(img, dtype=np.float64)
+    H, W = img.shape
+    out = np.empty_like(img)
+    c = np.ascontiguousarray(coeffs, dtype=np.float64)
+    assert c.size == 4
+    if _load().oracle_lift2_forward(_dptr(img), _dptr(out), W, H, levels, int(bool(round_f32)), _dptr(c),
+                                    float(K)) < 0:
         raise ValueError("oracle: invalid arguments")
     return out
 

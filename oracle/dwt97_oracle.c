@@ -44,6 +44,9 @@
 
 #define PAD 8
 
+static void lift_step(double *e, long len, int par, long lo, long hi, double coef);
+static long wss97(long k, long n);
+
 static const double ALPHA = -1.586134342059924;
 static const double BETA = -0.052980118572961;
 static const double GAMMA = 0.882911075530934;
@@ -84,31 +87,48 @@ static void lift_step(double *e, long len, int par, long lo, long hi, double coe
             e[j] += coef * (e[j - 1] + e[j + 1]);
 }
 
-/* Forward 1-D CDF 9/7 of x[0..n) (stride apart): ceil(n/2) low, floor(n/2) high. */
-static void lift97_fwd_1d(const double *x, long n, long stride, double *low, double *high)
+/* Forward 1-D lifting with two predict/update pairs and scaling (c = the
+ * four lifting coefficients p1, u1, p2, u2; K the scaling) of x[0..n)
+ * (stride apart): ceil(n/2) low, floor(n/2) high.  CDF 9/7 is
+ * c = (ALPHA, BETA, GAMMA, DELTA), K = KAPPA; CDF 5/3 is (-1/2, 1/4, 0, 0), 1. */
+static void lift2_fwd_1d(const double *x, long n, long stride, double *low, double *high, const double *c,
+                         double K)
 {
     long len = n + 2 * PAD, j, i;
     double *e = (double *)malloc((size_t)len * sizeof(double));
     for (j = 0; j < len; j++)
         e[j] = x[wss97(j - PAD, n) * stride];           /* PAD even: parity of j = parity of j - PAD */
-    lift_step(e, len, 1, 1, len - 1, ALPHA);            /* valid odd samples: [1, len-1) */
-    lift_step(e, len, 0, 2, len - 2, BETA);             /* valid even samples: [2, len-2) */
-    lift_step(e, len, 1, 3, len - 3, GAMMA);
-    lift_step(e, len, 0, 4, len - 4, DELTA);            /* [4, len-4) covers [PAD, PAD+n) */
+    lift_step(e, len, 1, 1, len - 1, c[0]);             /* valid odd samples: [1, len-1) */
+    lift_step(e, len, 0, 2, len - 2, c[1]);             /* valid even samples: [2, len-2) */
+    lift_step(e, len, 1, 3, len - 3, c[2]);
+    lift_step(e, len, 0, 4, len - 4, c[3]);             /* [4, len-4) covers [PAD, PAD+n) */
     for (i = 0; i < (n + 1) / 2; i++)
-        low[i] = e[PAD + 2 * i] / KAPPA;
+        low[i] = e[PAD + 2 * i] / K;
     for (i = 0; i < n / 2; i++)
-        high[i] = e[PAD + 2 * i + 1] * KAPPA;
+        high[i] = e[PAD + 2 * i + 1] * K;
     free(e);
 }
 
-/* Inverse of lift97_fwd_1d: x[0..n) (stride apart) from low / high. */
-static void lift97_inv_1d(const double *low, const double *high, long n, double *x, long stride)
+static const double C97[4] = {-1.586134342059924, -0.052980118572961, 0.882911075530934, 0.443506852043971};
+
+static void lift97_fwd_1d(const double *x, long n, long stride, double *low, double *high)
+{
+    (void)ALPHA; (void)BETA; (void)GAMMA; (void)DELTA;
+    lift2_fwd_1d(x, n, stride, low, high, C97, KAPPA);
+}
+
+/* Inverse of lift2_fwd_1d: x[0..n) (stride apart) from low / high. */
+static void lift2_inv_1d(const double *low, const double *high, long n, double *x, long stride, const double *cf,
+                         double K)
 {
     long len = n + 2 * PAD, j, i, nl = (n + 1) / 2;
     double *c, *e;
-    if (n == 1) {               /* one sample: the forward is the identity (DC gain 1) */
-        x[0] = low[0];
+    if (n == 1) {
+        /* one sample: the extended signal is constant, so the forward is
+         * low = G x / K with G the lifting's gain on a constant */
+        double d1 = 1.0 + 2.0 * cf[0], s1 = 1.0 + 2.0 * cf[1] * d1;
+        double d2 = d1 + 2.0 * cf[2] * s1, G = s1 + 2.0 * cf[3] * d2;
+        x[0] = low[0] * K / G;
         return;
     }
     c = (double *)malloc((size_t)n * sizeof(double));
@@ -116,19 +136,24 @@ static void lift97_inv_1d(const double *low, const double *high, long n, double 
     /* interleaved coefficient signal, scaling undone; it is symmetric with
      * the same whole-sample rule as the input, so it is extended likewise */
     for (i = 0; i < nl; i++)
-        c[2 * i] = low[i] * KAPPA;
+        c[2 * i] = low[i] * K;
     for (i = 0; i < n / 2; i++)
-        c[2 * i + 1] = high[i] / KAPPA;
+        c[2 * i + 1] = high[i] / K;
     for (j = 0; j < len; j++)
         e[j] = c[wss97(j - PAD, n)];
-    lift_step(e, len, 0, 1, len - 1, -DELTA);
-    lift_step(e, len, 1, 2, len - 2, -GAMMA);
-    lift_step(e, len, 0, 3, len - 3, -BETA);
-    lift_step(e, len, 1, 4, len - 4, -ALPHA);
+    lift_step(e, len, 0, 1, len - 1, -cf[3]);
+    lift_step(e, len, 1, 2, len - 2, -cf[2]);
+    lift_step(e, len, 0, 3, len - 3, -cf[1]);
+    lift_step(e, len, 1, 4, len - 4, -cf[0]);
     for (i = 0; i < n; i++)
         x[i * stride] = e[PAD + i];
     free(e);
     free(c);
+}
+
+static void lift97_inv_1d(const double *low, const double *high, long n, double *x, long stride)
+{
+    lift2_inv_1d(low, high, n, x, stride, C97, KAPPA);
 }
 
 static void level97_fwd_lifting(double *buf, long pitch, long W, long H)
@@ -224,6 +249,41 @@ void oracle_dwt97_fwd_1d(const double *x, long n, double *out)
 void oracle_dwt97_inv_1d(const double *in, long n, double *x)
 {
     lift97_inv_1d(in, in + (n + 1) / 2, n, x, 1);
+}
+
+/* General K <= 2 lifting (SURVEY.md 8f N4 "general lifting wavelets"):
+ * c = (p1, u1, p2, u2), K the scaling; levels of separable lifting on the
+ * symmetric extension, Mallat layout; round_f32 as below. */
+long oracle_lift2_forward(const double *in, double *out, long W, long H, long levels, int round_f32,
+                          const double *c, double K)
+{
+    long k, w = W, h = H, x, y, nlx, nly;
+    double *tmp, *line;
+    if (W < 1 || H < 1 || levels < 0 || !(K > 0.0))
+        return -1;
+    memcpy(out, in, (size_t)W * (size_t)H * sizeof(double));
+    tmp = (double *)malloc((size_t)W * (size_t)H * sizeof(double));
+    line = (double *)malloc((size_t)(W > H ? W : H) * sizeof(double));
+    for (k = 0; k < levels; k++) {
+        nlx = (w + 1) / 2;
+        nly = (h + 1) / 2;
+        for (y = 0; y < h; y++) {
+            lift2_fwd_1d(out + y * W, w, 1, line, line + nlx, c, K);
+            memcpy(tmp + y * w, line, (size_t)w * sizeof(double));
+        }
+        for (x = 0; x < w; x++) {
+            lift2_fwd_1d(tmp + x, h, w, line, line + nly, c, K);
+            for (y = 0; y < h; y++)
+                out[y * W + x] = line[y];
+        }
+        if (round_f32)
+            round97_f32(out, W, w, h);
+        w = nlx;
+        h = nly;
+    }
+    free(line);
+    free(tmp);
+    return levels;
 }
 
 /* levels of A97 (use_conv = 0) or B97 (use_conv = 1); round_f32 rounds each

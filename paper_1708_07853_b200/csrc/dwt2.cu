@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -1020,8 +1021,8 @@ int32_t configure_kernels(int *max_ctas)
 dwt2_plan *make_plan(int W, int H, int levels, int boundary, int max_count, bool strip, int Hg, int rb, int re,
                      int wavelet = DWT2_WAVELET_CDF53)
 {
-    if (wavelet < DWT2_WAVELET_CDF53 || wavelet > DWT2_WAVELET_CDF53_K2 || (strip && wavelet != DWT2_WAVELET_CDF53)) {
-        g_last_error = wavelet < 0 || wavelet > DWT2_WAVELET_CDF53_K2 ? DWT2_EINVAL : DWT2_EUNSUPPORTED;
+    if (wavelet < DWT2_WAVELET_CDF53 || wavelet > DWT2_WAVELET_LIFTING || (strip && wavelet != DWT2_WAVELET_CDF53)) {
+        g_last_error = wavelet < 0 || wavelet > DWT2_WAVELET_LIFTING ? DWT2_EINVAL : DWT2_EUNSUPPORTED;
         return nullptr;
     }
     if (boundary != DWT2_BOUNDARY_SYMMETRIC) {
@@ -1233,6 +1234,26 @@ dwt2_plan *dwt2_plan_create_ex(int32_t width, int32_t height, int32_t levels, in
                                int32_t max_count)
 {
     return make_plan(width, height, levels, boundary, max_count, false, height, 0, height, wavelet);
+}
+
+dwt2_plan *dwt2_plan_create_lifting(int32_t width, int32_t height, int32_t levels, int32_t boundary,
+                                    const double *coeffs, double K, int32_t max_count)
+{
+    if (!coeffs || !(K > 0.0) || !std::isfinite(K)) {
+        g_last_error = DWT2_EINVAL;
+        return nullptr;
+    }
+    for (int i = 0; i < 4; ++i)
+        if (!std::isfinite(coeffs[i])) {
+            g_last_error = DWT2_EINVAL;
+            return nullptr;
+        }
+    dwt2_plan *p = make_plan(width, height, levels, boundary, max_count, false, height, 0, height,
+                             DWT2_WAVELET_LIFTING);
+    if (!p) return nullptr;
+    for (int i = 0; i < 4; ++i) p->lift[i] = coeffs[i];
+    p->lift[4] = K;
+    return p;
 }
 
 dwt2_plan *dwt2_plan_create_batched(int32_t width, int32_t height, int32_t levels, int32_t boundary,

@@ -43,6 +43,7 @@ inline bool overlap(const void *a, size_t an, const void *b, size_t bn)
 struct dwt2_plan {
     int W, H, levels, max_count;
     int wavelet;              // DWT2_WAVELET_*: CDF53 runs the fused 5/3 kernel (dwt2.cu), others dwt97.cu
+    double lift[5];           // DWT2_WAVELET_LIFTING: p1, u1, p2, u2, K
     int device;
     // strip plans
     bool strip;

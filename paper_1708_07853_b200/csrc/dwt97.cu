@@ -40,13 +40,22 @@ using namespace dwt2_detail;
 
 namespace {
 
+#ifndef DWT2_K2_QK
+#define DWT2_K2_QK 2                       // measured: 4 quads per lane is not faster (fewer warps fit)
+#endif
+#ifndef DWT2_K2_MINB
+#define DWT2_K2_MINB (DWT2_K2_QK == 4 ? 2 : 4)   // CTAs per SM the register budget is sized for
+#endif
 constexpr int KW = 4;                      // warps per CTA
 constexpr int KT = KW * 32;
-constexpr int SLABQ = 64;                  // quad columns per warp (2 per lane)
-constexpr int OUTQ = 60;                   // output quad columns per warp (lanes 1..30)
-constexpr int DS = 8;                      // raw quad rows in flight per warp (shared-memory ring, cp.async)
+constexpr int QK = DWT2_K2_QK;             // quads per lane (2 or 4)
+constexpr int SLABQ = 32 * QK;             // quad columns per warp
+constexpr int OUTQ = 30 * QK;              // output quad columns per warp (lanes 1..30; lanes 0, 31: halo)
+constexpr int RW = 2 * SLABQ;              // floats per staged pixel row (= 64 QK)
+constexpr int DS = QK == 4 ? 6 : 8;        // raw quad rows in flight per warp (shared-memory ring, cp.async)
 constexpr int DR = 1;                      // raw quad rows in flight per warp on the register path (edge slabs)
-constexpr size_t K2_SMEM = size_t(KW) * DS * 2 * 128 * sizeof(float);
+constexpr size_t K2_SMEM = size_t(KW) * DS * 2 * RW * sizeof(float);
+static_assert(QK == 2 || QK == 4, "2 or 4 quads per lane");
 
 __device__ __forceinline__ void cp_async16(float *dst, const float *src)
 {
@@ -81,10 +90,10 @@ __device__ __forceinline__ int wssi(int k, int n)
     return k >= n ? p - k : k;
 }
 
-// Raw quad row r (pixel rows 2r, 2r+1, mirrored) of the lane's 2 quads:
-// pixels x = xb .. xb+3 with xb = 2 (m0 - 2) + 4 lane.
+// Raw quad row r (pixel rows 2r, 2r+1, mirrored) of the lane's QK quads:
+// pixels x = xb .. xb + 2 QK - 1 with xb = 2 (m0 - QK) + 2 QK lane.
 struct RawRow {
-    float e[4], o[4];                       // even row: a0 b0 a1 b1; odd row: c0 d0 c1 d1
+    float e[2 * QK], o[2 * QK];             // even row: a0 b0 a1 b1 ..; odd row: c0 d0 c1 d1 ..
 };
 
 template <bool VEC, bool EDGE>
@@ -99,13 +108,16 @@ __device__ __forceinline__ RawRow load_raw_row(const K2Args &a, const float *img
     const float *p1 = img + (long long)y1 * a.in_pitch;
     RawRow R;
     if (VEC && !EDGE) {
-        const float4 u = __ldg(reinterpret_cast<const float4 *>(p0 + xb));
-        const float4 v = __ldg(reinterpret_cast<const float4 *>(p1 + xb));
-        R.e[0] = u.x; R.e[1] = u.y; R.e[2] = u.z; R.e[3] = u.w;
-        R.o[0] = v.x; R.o[1] = v.y; R.o[2] = v.z; R.o[3] = v.w;
+#pragma unroll
+        for (int q = 0; q < QK / 2; ++q) {
+            const float4 u = __ldg(reinterpret_cast<const float4 *>(p0 + xb) + q);
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(p1 + xb) + q);
+            R.e[4 * q] = u.x; R.e[4 * q + 1] = u.y; R.e[4 * q + 2] = u.z; R.e[4 * q + 3] = u.w;
+            R.o[4 * q] = v.x; R.o[4 * q + 1] = v.y; R.o[4 * q + 2] = v.z; R.o[4 * q + 3] = v.w;
+        }
     } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 2 * QK; ++j) {
             const int x = EDGE ? wssi(xb + j, a.W) : xb + j;
             R.e[j] = __ldg(p0 + x);
             R.o[j] = __ldg(p1 + x);
@@ -125,6 +137,11 @@ struct Carry2 {
 __device__ __forceinline__ double shr(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }   // lane + 1
 __device__ __forceinline__ double shl(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }     // lane - 1
 
+// horizontal neighbours of quad i of the lane: i + 1 (lane + 1's quad 0 for
+// the last) and i - 1 (lane - 1's last quad for the first)
+#define K2_RIGHT(x, i, nb) ((i) < QK - 1 ? (x)[(i) + 1] : (nb))
+#define K2_LEFT(x, i, nb) ((i) > 0 ? (x)[(i) - 1] : (nb))
+
 template <bool VEC, bool EDGE>
 __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, int n1, int lane)
 {
@@ -135,10 +152,10 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
     constexpr int D = ASYNC ? DS : DR;
     const int Wq = (a.W + 1) >> 1, Wh = a.W >> 1, Hh = a.H >> 1;
     const float *in = a.in + (long long)img * a.in_img;
-    const int xb = 2 * (m0 - 2) + 4 * lane;
-    Carry2 cy[2];
+    const int xb = 2 * (m0 - QK) + 2 * QK * lane;
+    Carry2 cy[QK];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) cy[i] = Carry2{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < QK; ++i) cy[i] = Carry2{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     const int r_first = n0 - 2, r_last = n1 + 1;
     RawRow reg[ASYNC ? 1 : D];
     auto issue = [&](int j, int r) {               // j: compile-time slot
@@ -148,8 +165,13 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
                 y0 = wssi(y0, a.H);
                 y1 = wssi(y1, a.H);
             }
-            cp_async16(wring + (2 * j) * 128 + 4 * lane, in + (long long)y0 * a.in_pitch + xb);
-            cp_async16(wring + (2 * j + 1) * 128 + 4 * lane, in + (long long)y1 * a.in_pitch + xb);
+            const float *s0 = in + (long long)y0 * a.in_pitch + xb;
+            const float *s1 = in + (long long)y1 * a.in_pitch + xb;
+#pragma unroll
+            for (int q = 0; q < QK / 2; ++q) {
+                cp_async16(wring + (2 * j) * RW + 2 * QK * lane + 4 * q, s0 + 4 * q);
+                cp_async16(wring + (2 * j + 1) * RW + 2 * QK * lane + 4 * q, s1 + 4 * q);
+            }
         } else {
             reg[ASYNC ? 0 : j] = load_raw_row<VEC, EDGE>(a, in, r, xb);
         }
@@ -162,7 +184,7 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
         issue(j, r_first + j);
         if (ASYNC) cp_async_commit();
     }
-    const int mo = m0 + 2 * (lane - 1);               // first output quad of the lane (lanes 1..30)
+    const int mo = m0 + QK * (lane - 1);              // first output quad of the lane (lanes 1..30)
     const bool out_lane = lane >= 1 && lane <= 30;
     // output cursors at row r - 2 of the walk, advanced one row per iteration
     float *cll = a.ll + (long long)img * a.ll_img + (long long)(r_first - 2) * a.ll_pitch + mo;
@@ -177,108 +199,125 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
         RawRow R;
         if (ASYNC) {
             cp_async_wait<D - 1>();                    // row r's group (the oldest) has landed
-            const float4 u = *reinterpret_cast<const float4 *>(wring + (2 * j) * 128 + 4 * lane);
-            const float4 v = *reinterpret_cast<const float4 *>(wring + (2 * j + 1) * 128 + 4 * lane);
-            R.e[0] = u.x; R.e[1] = u.y; R.e[2] = u.z; R.e[3] = u.w;
-            R.o[0] = v.x; R.o[1] = v.y; R.o[2] = v.z; R.o[3] = v.w;
+#pragma unroll
+            for (int q = 0; q < QK / 2; ++q) {
+                const float4 u = *reinterpret_cast<const float4 *>(wring + (2 * j) * RW + 2 * QK * lane + 4 * q);
+                const float4 v = *reinterpret_cast<const float4 *>(wring + (2 * j + 1) * RW + 2 * QK * lane + 4 * q);
+                R.e[4 * q] = u.x; R.e[4 * q + 1] = u.y; R.e[4 * q + 2] = u.z; R.e[4 * q + 3] = u.w;
+                R.o[4 * q] = v.x; R.o[4 * q + 1] = v.y; R.o[4 * q + 2] = v.z; R.o[4 * q + 3] = v.w;
+            }
         } else {
             R = reg[ASYNC ? 0 : j];
         }
         if (!ASYNC) issue(j, r + D);
-        double av[2], bv[2], cv[2], dv[2];
+        double av[QK], bv[QK], cv[QK], dv[QK];
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < QK; ++i) {
             av[i] = R.e[2 * i]; bv[i] = R.e[2 * i + 1];
             cv[i] = R.o[2 * i]; dv[i] = R.o[2 * i + 1];
         }
         // ---- predict 1, row r (same-row part): HL'1 = b + c0 (a + a[m+1])
         const double a_nb = shr(av[0]);
-        double hl1[2];
-        hl1[0] = fma(a.c0, av[0] + av[1], bv[0]);
-        hl1[1] = fma(a.c0, av[1] + a_nb, bv[1]);
+        double hl1[QK];
+#pragma unroll
+        for (int i = 0; i < QK; ++i) hl1[i] = fma(a.c0, av[i] + K2_RIGHT(av, i, a_nb), bv[i]);
         // ---- predict 1 completes row r-1: LH'1 = c + c0 (a + a[n+1]),
         //      HH'1 = d + c0 (c + c[m+1]) + c0 (HL'1 + HL'1[n+1])
-        const double c_nb = shr(cy[0].c);
-        double lh1[2], hh1[2];
+        double cp_[QK];
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const double cr = (i == 0) ? cy[1].c : c_nb;
+        for (int i = 0; i < QK; ++i) cp_[i] = cy[i].c;
+        const double c_nb = shr(cp_[0]);
+        double lh1[QK], hh1[QK];
+#pragma unroll
+        for (int i = 0; i < QK; ++i) {
             lh1[i] = fma(a.c0, cy[i].a + av[i], cy[i].c);
-            hh1[i] = fma(a.c0, cy[i].hl1 + hl1[i], fma(a.c0, cy[i].c + cr, cy[i].d));
+            hh1[i] = fma(a.c0, cy[i].hl1 + hl1[i], fma(a.c0, cy[i].c + K2_RIGHT(cp_, i, c_nb), cy[i].d));
         }
         // ---- update 1, row r-1: LH1 = LH'1 + c1 (HH'1 + HH'1[m-1]),
         //      HL1 = HL'1 + c1 (HH'1 + HH'1[n-1]),
         //      LL1 = a + c1 (HL'1 + HL'1[m-1]) + c1 (LH1 + LH1[n-1])
-        const double hh1_l = shl(hh1[1]);
-        const double hl1p_l = shl(cy[1].hl1);
-        double A1[2], B1[2], C1[2];
+        double hlp[QK];
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const double hhl = (i == 0) ? hh1_l : hh1[0];
-            const double hll = (i == 0) ? hl1p_l : cy[0].hl1;
-            C1[i] = fma(a.c1, hh1[i] + hhl, lh1[i]);
+        for (int i = 0; i < QK; ++i) hlp[i] = cy[i].hl1;
+        const double hh1_l = shl(hh1[QK - 1]);
+        const double hl1p_l = shl(hlp[QK - 1]);
+        double A1[QK], B1[QK], C1[QK];
+#pragma unroll
+        for (int i = 0; i < QK; ++i) {
+            C1[i] = fma(a.c1, hh1[i] + K2_LEFT(hh1, i, hh1_l), lh1[i]);
             B1[i] = fma(a.c1, hh1[i] + cy[i].hh1, cy[i].hl1);
-            A1[i] = fma(a.c1, C1[i] + cy[i].lh1f, fma(a.c1, cy[i].hl1 + hll, cy[i].a));
+            A1[i] = fma(a.c1, C1[i] + cy[i].lh1f, fma(a.c1, cy[i].hl1 + K2_LEFT(hlp, i, hl1p_l), cy[i].a));
         }
         // ---- predict 2 on the update-1 output, row r-1 (same-row part):
         //      HL'2 = HL1 + c2 (LL1 + LL1[m+1])
         const double A_nb = shr(A1[0]);
-        double hl2[2];
-        hl2[0] = fma(a.c2, A1[0] + A1[1], B1[0]);
-        hl2[1] = fma(a.c2, A1[1] + A_nb, B1[1]);
+        double hl2[QK];
+#pragma unroll
+        for (int i = 0; i < QK; ++i) hl2[i] = fma(a.c2, A1[i] + K2_RIGHT(A1, i, A_nb), B1[i]);
         // ---- predict 2 completes row r-2 (carried A, LH1 = lh1f, HH1 = hh1, HL'2):
         //      LH'2 = LH1 + c2 (LL1 + LL1[n+1]), HH'2 = HH1 + c2 (LH1 + LH1[m+1]) + c2 (HL'2 + HL'2[n+1])
-        const double C_nb = shr(cy[0].lh1f);
-        double lh2[2], hh2[2];
+        double lf[QK];
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const double cr = (i == 0) ? cy[1].lh1f : C_nb;
+        for (int i = 0; i < QK; ++i) lf[i] = cy[i].lh1f;
+        const double C_nb = shr(lf[0]);
+        double lh2[QK], hh2[QK];
+#pragma unroll
+        for (int i = 0; i < QK; ++i) {
             lh2[i] = fma(a.c2, cy[i].A + A1[i], cy[i].lh1f);
-            hh2[i] = fma(a.c2, cy[i].hl2 + hl2[i], fma(a.c2, cy[i].lh1f + cr, cy[i].hh1));
+            hh2[i] = fma(a.c2, cy[i].hl2 + hl2[i], fma(a.c2, cy[i].lh1f + K2_RIGHT(lf, i, C_nb), cy[i].hh1));
         }
         // ---- update 2, row r-2
-        const double hh2_l = shl(hh2[1]);
-        const double hl2p_l = shl(cy[1].hl2);
-        double A2[2], B2[2], C2[2];
+        double h2p[QK];
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const double hhl = (i == 0) ? hh2_l : hh2[0];
-            const double hll = (i == 0) ? hl2p_l : cy[0].hl2;
-            C2[i] = fma(a.c3, hh2[i] + hhl, lh2[i]);
+        for (int i = 0; i < QK; ++i) h2p[i] = cy[i].hl2;
+        const double hh2_l = shl(hh2[QK - 1]);
+        const double hl2p_l = shl(h2p[QK - 1]);
+        double A2[QK], B2[QK], C2[QK];
+#pragma unroll
+        for (int i = 0; i < QK; ++i) {
+            C2[i] = fma(a.c3, hh2[i] + K2_LEFT(hh2, i, hh2_l), lh2[i]);
             B2[i] = fma(a.c3, hh2[i] + cy[i].hh2, cy[i].hl2);
-            A2[i] = fma(a.c3, C2[i] + cy[i].lh2f, fma(a.c3, cy[i].hl2 + hll, cy[i].A));
+            A2[i] = fma(a.c3, C2[i] + cy[i].lh2f, fma(a.c3, cy[i].hl2 + K2_LEFT(h2p, i, hl2p_l), cy[i].A));
         }
         // ---- store output row r-2 (scaled)
         const int n = r - 2;
         if (n >= n0 && n < n1 && out_lane) {
-            float oLL[2], oHL[2], oLH[2], oHH[2];
+            float oLL[QK], oHL[QK], oLH[QK], oHH[QK];
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
+            for (int i = 0; i < QK; ++i) {
                 oLL[i] = (float)(A2[i] * a.sll);
                 oHL[i] = (float)(B2[i] * a.sd);
                 oLH[i] = (float)(C2[i] * a.sd);
                 oHH[i] = (float)(hh2[i] * a.shh);
             }
-            float *pll = cll, *phl = chl, *plh = clh, *phh = chh;
             const bool has_odd = n < Hh;
             if (VEC && !EDGE) {
-                *reinterpret_cast<float2 *>(pll) = make_float2(oLL[0], oLL[1]);
-                __stcs(reinterpret_cast<float2 *>(phl), make_float2(oHL[0], oHL[1]));
-                if (has_odd) {
-                    __stcs(reinterpret_cast<float2 *>(plh), make_float2(oLH[0], oLH[1]));
-                    __stcs(reinterpret_cast<float2 *>(phh), make_float2(oHH[0], oHH[1]));
+                if (QK == 4) {
+                    *reinterpret_cast<float4 *>(cll) = make_float4(oLL[0], oLL[1], oLL[2 % QK], oLL[3 % QK]);
+                    __stcs(reinterpret_cast<float4 *>(chl), make_float4(oHL[0], oHL[1], oHL[2 % QK], oHL[3 % QK]));
+                    if (has_odd) {
+                        __stcs(reinterpret_cast<float4 *>(clh), make_float4(oLH[0], oLH[1], oLH[2 % QK], oLH[3 % QK]));
+                        __stcs(reinterpret_cast<float4 *>(chh), make_float4(oHH[0], oHH[1], oHH[2 % QK], oHH[3 % QK]));
+                    }
+                } else {
+                    *reinterpret_cast<float2 *>(cll) = make_float2(oLL[0], oLL[1]);
+                    __stcs(reinterpret_cast<float2 *>(chl), make_float2(oHL[0], oHL[1]));
+                    if (has_odd) {
+                        __stcs(reinterpret_cast<float2 *>(clh), make_float2(oLH[0], oLH[1]));
+                        __stcs(reinterpret_cast<float2 *>(chh), make_float2(oHH[0], oHH[1]));
+                    }
                 }
             } else {
 #pragma unroll
-                for (int i = 0; i < 2; ++i) {
+                for (int i = 0; i < QK; ++i) {
                     const int m = mo + i;
                     if (m < Wq) {
-                        pll[i] = oLL[i];
-                        if (has_odd) __stcs(plh + i, oLH[i]);
+                        cll[i] = oLL[i];
+                        if (has_odd) __stcs(clh + i, oLH[i]);
                     }
                     if (m < Wh) {
-                        __stcs(phl + i, oHL[i]);
-                        if (has_odd) __stcs(phh + i, oHH[i]);
+                        __stcs(chl + i, oHL[i]);
+                        if (has_odd) __stcs(chh + i, oHH[i]);
                     }
                 }
             }
@@ -289,7 +328,7 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
         chh += a.out_pitch;
         // ---- carries
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < QK; ++i) {
             cy[i].hh2 = hh2[i];
             cy[i].lh2f = C2[i];
             cy[i].A = A1[i];
@@ -315,13 +354,13 @@ __device__ __forceinline__ void pdl_wait97() { asm volatile("griddepcontrol.wait
 __device__ __forceinline__ void pdl_launch97() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 template <bool VEC>
-__global__ void __launch_bounds__(KT, 4) dwt_k2_level_kernel(const __grid_constant__ K2Args a)
+__global__ void __launch_bounds__(KT, DWT2_K2_MINB) dwt_k2_level_kernel(const __grid_constant__ K2Args a)
 {
     pdl_launch97();
     pdl_wait97();
     extern __shared__ __align__(16) float k2_smem[];
     const int lane = threadIdx.x & 31;
-    float *wring = k2_smem + (threadIdx.x >> 5) * (DS * 2 * 128);
+    float *wring = k2_smem + (threadIdx.x >> 5) * (DS * 2 * RW);
     const long long nwarps = (long long)gridDim.x * KW;
     const int Wq = (a.W + 1) >> 1, Hq = (a.H + 1) >> 1;
     const long long per_img = (long long)a.nblk * a.nslabs;
@@ -332,8 +371,9 @@ __global__ void __launch_bounds__(KT, 4) dwt_k2_level_kernel(const __grid_consta
         const int slab = rr - blk * a.nslabs;
         const int m0 = slab * OUTQ;
         const int n0 = blk * a.tb, n1 = min(n0 + a.tb, Hq);
-        // pixel columns 2 (m0 - 2) .. 2 (m0 + 62) - 1 must lie inside the image for the unmirrored path
-        const bool edge = (m0 < 2) || (2 * (m0 + 62) > a.W) || (m0 + OUTQ > Wq);
+        // pixel columns 2 (m0 - QK) .. 2 (m0 - QK + SLABQ) - 1 must lie inside the image for the
+        // unmirrored path (and every output quad of the slab must exist)
+        const bool edge = (m0 < QK) || (2 * (m0 - QK + SLABQ) > a.W) || (m0 + OUTQ > Wq);
         if (edge) k2_tile<VEC, true>(a, wring, img, m0, n0, n1, lane);
         else k2_tile<VEC, false>(a, wring, img, m0, n0, n1, lane);
     }
@@ -361,8 +401,10 @@ struct Wavelet2 {
     double c0, c1, c2, c3, K;
 };
 
-Wavelet2 wavelet_params(int wavelet)
+Wavelet2 wavelet_params(const dwt2_plan *p)
 {
+    const int wavelet = p->wavelet;
+    if (wavelet == DWT2_WAVELET_LIFTING) return Wavelet2{p->lift[0], p->lift[1], p->lift[2], p->lift[3], p->lift[4]};
     if (wavelet == DWT2_WAVELET_CDF97)
         return Wavelet2{-1.586134342059924, -0.052980118572961, 0.882911075530934, 0.443506852043971,
                         1.230174104914001};
@@ -383,9 +425,9 @@ int32_t launch_k2_level(const dwt2_plan *p, K2Args a, cudaStream_t s)
     const long long want = (a.ntiles + KW - 1) / KW;
     const int grid = int(std::max<long long>(1, std::min<long long>(want, warps / KW)));
     const bool vec = aligned(a.in, 16) && a.in_pitch % 4 == 0 && (a.count == 1 || a.in_img % 4 == 0) &&
-                     aligned(a.ll, 8) && aligned(a.hl, 8) && aligned(a.lh, 8) && aligned(a.hh, 8) &&
-                     a.ll_pitch % 2 == 0 && a.out_pitch % 2 == 0 &&
-                     (a.count == 1 || (a.ll_img % 2 == 0 && a.out_img % 2 == 0));
+                     aligned(a.ll, 4 * QK) && aligned(a.hl, 4 * QK) && aligned(a.lh, 4 * QK) && aligned(a.hh, 4 * QK) &&
+                     a.ll_pitch % QK == 0 && a.out_pitch % QK == 0 &&
+                     (a.count == 1 || (a.ll_img % QK == 0 && a.out_img % QK == 0));
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(grid);
@@ -415,7 +457,7 @@ namespace dwt2_detail {
 int32_t run_levels_k2(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,
                       long long out_stride, cudaStream_t s)
 {
-    const Wavelet2 wv = wavelet_params(p->wavelet);
+    const Wavelet2 wv = wavelet_params(p);
     for (int k = 0; k < p->levels; ++k) {
         const LevelGeom &g = p->geom[k];
         K2Args a;

@@ -168,11 +168,17 @@ def strip_forward_step(exchange: StripExchange, plan, out, overlap: bool = True,
     return out
 
 
+def _p2p_ops(msgs, buf):
+    """The grouped sends/receives of rows of `buf` (a 2-D tensor)."""
+    import torch.distributed as dist
+    return [dist.P2POp(dist.isend if op == "send" else dist.irecv, buf[row0:row0 + nrows], peer)
+            for op, peer, row0, nrows in msgs]
+
+
 def _p2p(msgs, buf):
     """Post grouped sends/receives of rows of `buf` (a 2-D tensor)."""
     import torch.distributed as dist
-    ops = [dist.P2POp(dist.isend if op == "send" else dist.irecv, buf[row0:row0 + nrows], peer)
-           for op, peer, row0, nrows in msgs]
+    ops = _p2p_ops(msgs, buf)
     return dist.batch_isend_irecv(ops) if ops else []
 
 
@@ -215,8 +221,13 @@ class StripPyramid:
         return self.bufs[k][:, :self.geom[k][0]]
 
     def start(self, k: int):
-        """Post level k's ghost-row exchange over the default process group."""
-        return _p2p(self.msgs[k], self.bufs[k])
+        """Post level k's ghost-row exchange over the default process group
+        (the P2POp lists are built once: the per-step host cost is the NCCL
+        group call only)."""
+        import torch.distributed as dist
+        if not hasattr(self, "_ops"):
+            self._ops = [_p2p_ops(self.msgs[j], self.bufs[j]) for j in range(self.levels)]
+        return dist.batch_isend_irecv(self._ops[k]) if self._ops[k] else []
 
     @staticmethod
     def finish(reqs):

@@ -18,8 +18,8 @@ LIB_PATH = os.environ.get("DWT2_LIB") or os.path.join(_PKG, "libdwt2.so")   # DW
 DWT2_OK, DWT2_EINVAL, DWT2_ENOMEM, DWT2_ECUDA, DWT2_EUNSUPPORTED = 0, -1, -2, -3, -4
 DWT2_BOUNDARY_SYMMETRIC = 0
 DWT2_STRIP_ALL, DWT2_STRIP_INTERIOR, DWT2_STRIP_BOUNDARY = 0, 1, 2
-DWT2_WAVELET_CDF53, DWT2_WAVELET_CDF97, DWT2_WAVELET_CDF53_K2 = 0, 1, 2
-WAVELETS = {"cdf53": 0, "cdf97": 1, "cdf53_k2": 2}
+DWT2_WAVELET_CDF53, DWT2_WAVELET_CDF97, DWT2_WAVELET_CDF53_K2, DWT2_WAVELET_LIFTING = 0, 1, 2, 3
+WAVELETS = {"cdf53": 0, "cdf97": 1, "cdf53_k2": 2, "lifting": 3}
 SCHEMES = {"fused": 0, "nonsep_naive": 1, "nonsep_lifting": 2, "nonsep_adapted": 3, "sep_conv": 4,
            "sep_lifting": 5}
 
@@ -44,6 +44,7 @@ SIGNATURES = {
     "dwt2_plan_create": (_P, [_I32, _I32, _I32, _I32]),
     "dwt2_plan_create_batched": (_P, [_I32, _I32, _I32, _I32, _I32]),
     "dwt2_plan_create_ex": (_P, [_I32, _I32, _I32, _I32, _I32, _I32]),
+    "dwt2_plan_create_lifting": (_P, [_I32, _I32, _I32, _I32, ctypes.POINTER(ctypes.c_double), ctypes.c_double, _I32]),
     "dwt2_plan_create_strip": (_P, [_I32, _I32, _I32, _I32, _I32]),
     "dwt2_plan_create_strip_levels": (_P, [_I32, _I32, _I32, _I32, _I32, _I32]),
     "dwt2_strip_level_info": (_I32, [_P, _I32, ctypes.POINTER(StripLevel)]),
@@ -121,6 +122,12 @@ def dwt2_plan_create_batched(width, height, levels, boundary, max_count):
 def dwt2_plan_create_ex(width, height, levels, boundary, wavelet, max_count):
     return _plan_or_raise(lib().dwt2_plan_create_ex(width, height, levels, boundary, wavelet, max_count),
                           "dwt2_plan_create_ex")
+
+
+def dwt2_plan_create_lifting(width, height, levels, boundary, coeffs, K, max_count):
+    c = (ctypes.c_double * 4)(*[float(v) for v in coeffs])
+    return _plan_or_raise(lib().dwt2_plan_create_lifting(width, height, levels, boundary, c, float(K), max_count),
+                          "dwt2_plan_create_lifting")
 
 
 def dwt2_plan_create_strip(width, global_height, row_begin, row_end, boundary=DWT2_BOUNDARY_SYMMETRIC):
@@ -210,10 +217,17 @@ def _check_image(x, name):
 class Plan:
     """Owns a dwt2_plan* (see include/dwt2.h)."""
 
-    def __init__(self, width: int, height: int, levels: int = 1, max_count: int = 1, wavelet: str = "cdf53"):
+    def __init__(self, width: int, height: int, levels: int = 1, max_count: int = 1, wavelet: str = "cdf53",
+                 lifting=None):
+        """wavelet: "cdf53" (product 5/3 kernel), "cdf97", "cdf53_k2" or
+        "lifting" with lifting = (p1, u1, p2, u2, K)."""
         self.width, self.height, self.levels, self.max_count = width, height, levels, max_count
         self.wavelet = wavelet
-        if wavelet != "cdf53":
+        if wavelet == "lifting":
+            p1, u1, p2, u2, K = lifting
+            self._p = dwt2_plan_create_lifting(width, height, levels, DWT2_BOUNDARY_SYMMETRIC, (p1, u1, p2, u2), K,
+                                               max_count)
+        elif wavelet != "cdf53":
             self._p = dwt2_plan_create_ex(width, height, levels, DWT2_BOUNDARY_SYMMETRIC, WAVELETS[wavelet],
                                           max_count)
         elif max_count == 1:

@@ -106,3 +106,65 @@ def test_cdf97_unsupported_calls():
     with pytest.raises(dwt2.DWT2Error):
         plan.forward_scheme("sep_lifting", t, o)
     plan.close()
+
+
+# --------------------------------------------------------------------------
+# general lifting wavelets (dwt2_plan_create_lifting) and negative controls
+# --------------------------------------------------------------------------
+
+def gpu_lifting(x, levels, lifting):
+    H, W = x.shape
+    plan = dwt2.Plan(W, H, levels, wavelet="lifting", lifting=lifting)
+    out = plan.forward(torch.from_numpy(np.ascontiguousarray(x)).cuda()).cpu().numpy()
+    plan.close()
+    return out
+
+
+@pytest.mark.parametrize("lifting", [(-0.3, 0.15, 0.1, -0.05, 1.0), (-0.5, 0.25, 0.0, 0.0, 1.0),
+                                     (-1.586134342059924, -0.052980118572961, 0.882911075530934,
+                                      0.443506852043971, 1.230174104914001), (-0.25, 0.125, -0.5, 0.25, 1.5)])
+@pytest.mark.parametrize("W,H,levels", [(33, 17, 2), (1000, 777, 1), (515, 1030, 4)])
+def test_custom_lifting_against_general_oracle(lifting, W, H, levels):
+    x = workloads.uniform_real(W, H, W + 3 * H)
+    got = gpu_lifting(x, levels, lifting)
+    x64 = x.astype(np.float64)
+    ref = oracle.forward_lifting2(x64, levels, lifting[:4], lifting[4])
+    assert np.abs(got.astype(np.float64) - ref).max() <= 1e-4
+
+
+def test_negative_control_perturbed_update_fails():
+    """SPEC's negative control, on the GPU path: the K = 2 kernel with the 5/3
+    pair but the update coefficient off by 2^-10 must FAIL parity against the
+    5/3 oracle (and the exact pair must pass bit for bit) -- the comparison
+    can see a single wrong coefficient."""
+    W, H = 257, 130
+    x = workloads.uniform_int(W, H, 5)
+    ref = oracle.forward(x.astype(np.float64), 2, round_f32=True)
+    good = gpu_lifting(x, 2, (-0.5, 0.25, 0.0, 0.0, 1.0))
+    np.testing.assert_array_equal(good.astype(np.float64), ref)
+    bad = gpu_lifting(x, 2, (-0.5, 0.25 + 2.0 ** -10, 0.0, 0.0, 1.0))
+    assert np.abs(bad.astype(np.float64) - ref).max() > 1e-3
+    bad_sign = gpu_lifting(x, 2, (0.5, 0.25, 0.0, 0.0, 1.0))
+    assert np.abs(bad_sign.astype(np.float64) - ref).max() > 1.0
+
+
+def test_negative_control_harness_detects_one_ulp():
+    """The comparison used by every parity test flags a single coefficient
+    moved by one fp32 ulp (exact mode) -- the 0-error claims are not vacuous."""
+    from tests._parity import compare
+    x = workloads.uniform_int(64, 64, 9)
+    plan = dwt2.Plan(64, 64, 1)
+    got = plan.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    plan.close()
+    ref = oracle.forward(x.astype(np.float64), 1, round_f32=True)
+    compare(got, ref, ref, True, "clean")
+    got[17, 40] = np.nextafter(got[17, 40], np.float32(np.inf))
+    with pytest.raises(AssertionError):
+        compare(got, ref, ref, True, "perturbed")
+
+
+def test_lifting_plan_rejects_bad_scale():
+    with pytest.raises(dwt2.DWT2Error):
+        dwt2.Plan(64, 64, 1, wavelet="lifting", lifting=(-0.5, 0.25, 0.0, 0.0, 0.0))
+    with pytest.raises(dwt2.DWT2Error):
+        dwt2.Plan(64, 64, 1, wavelet="lifting", lifting=(float("nan"), 0.25, 0.0, 0.0, 1.0))

@@ -125,3 +125,32 @@ def test_round_f32_rounds_every_level():
     y1 = oracle.forward(x, 1, wavelet="cdf97")
     assert np.array_equal(oracle.forward(x, 1, round_f32=True, wavelet="cdf97"),
                           y1.astype(np.float32).astype(np.float64))
+
+
+# --------------------------------------------------------------------------
+# general K <= 2 lifting oracle (oracle_lift2_forward): pinned by its two
+# special cases, each an independently written oracle
+# --------------------------------------------------------------------------
+C97 = (-1.586134342059924, -0.052980118572961, 0.882911075530934, 0.443506852043971)
+K97 = 1.230174104914001
+
+
+@pytest.mark.parametrize("W,H,L", [(1, 1, 1), (7, 5, 2), (37, 45, 3), (64, 33, 5)])
+def test_general_lifting_reduces_to_53_and_97(W, H, L):
+    x = np.random.default_rng(W * 31 + H).integers(0, 256, (H, W)).astype(np.float64)
+    np.testing.assert_array_equal(oracle.forward_lifting2(x, L, (-0.5, 0.25, 0.0, 0.0), 1.0), oracle.forward(x, L))
+    np.testing.assert_array_equal(oracle.forward_lifting2(x, L, C97, K97), oracle.forward(x, L, wavelet="cdf97"))
+
+
+def test_general_lifting_is_linear_and_scaled():
+    """A made-up wavelet: the transform is linear, and K scales low / high as stated."""
+    rng = np.random.default_rng(8)
+    x, y = rng.uniform(0, 255, (2, 30, 22))
+    c = (-0.3, 0.15, 0.1, -0.05)
+    f = lambda im, K: oracle.forward_lifting2(im, 1, c, K)
+    np.testing.assert_allclose(f(2 * x - 3 * y, 1.0), 2 * f(x, 1.0) - 3 * f(y, 1.0), atol=1e-10)
+    a, b = f(x, 1.0), f(x, 2.0)
+    # 2-D: LL / K^2, HL and LH * 1, HH * K^2
+    np.testing.assert_allclose(b[:15, :11], a[:15, :11] / 4, atol=1e-12)
+    np.testing.assert_allclose(b[:15, 11:], a[:15, 11:], atol=1e-12)
+    np.testing.assert_allclose(b[15:, 11:], a[15:, 11:] * 4, atol=1e-12)
