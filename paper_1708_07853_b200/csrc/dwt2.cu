@@ -621,14 +621,16 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
             // one 1-D bulk copy per box row (cp.async.bulk, 16-byte granules)
             // of the 140 floats from the row's 16-byte-aligned address at or
             // below column x0 + BOX0 (the consumer re-derives the shift).  Lane
-            // i < NBOX * BOXH copies row i.  Clamped to [in, in_end): the first
-            // bytes of the buffer start at `in` (4 floats later in smem; the
-            // skipped columns lie left of the image and are never read), and
-            // the last < 16 bytes of the buffer are copied by lane 0 with plain
-            // loads before its arrive.  Rows outside the buffer are not copied.
+            // i < NBOX * BOXH copies row i.  The bulk copies stay inside the
+            // 16-byte-aligned part [lo16, hi16) of the buffer [in, in_end); the
+            // row's lane copies the < 16-byte head [in, lo16) and tail
+            // [hi16, in_end) with plain loads before lane 0's arrive (bytes left
+            // of `in` are never read: they lie left of the image).  Rows outside
+            // the buffer are not copied.
             const float *img_in = a.in + (long long)pt.img * a.in_img_stride;
             const uintptr_t lo = reinterpret_cast<uintptr_t>(a.in);
             const uintptr_t hi = reinterpret_cast<uintptr_t>(a.in_end);
+            const uintptr_t lo16 = (lo + 15) & ~uintptr_t(15);     // bulk copies stay inside [lo16, hi16)
             const uintptr_t hi16 = hi & ~uintptr_t(15);
             uint32_t my_bytes = 0;
             uintptr_t my_src = 0;
@@ -641,9 +643,11 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
                     uintptr_t st = reinterpret_cast<uintptr_t>(rowp) & ~uintptr_t(15);
                     uintptr_t en = st + 4 * Lay<false>::RP;
                     float *d = dst + bx * Lay<false>::SUB + rr * Lay<false>::RP;
-                    if (st < lo) {                  // left of the buffer start
-                        d += (lo - st) / 4;
-                        st = lo;
+                    if (st < lo16) {                // at the buffer start: [lo, lo16) by plain loads
+                        for (uintptr_t q = (st > lo ? st : lo); q < lo16 && q < en; q += 4)
+                            d[(q - st) / 4] = *reinterpret_cast<const float *>(q);
+                        d += (lo16 - st) / 4;
+                        st = lo16;
                     }
                     if (en > hi16) en = hi16;       // the < 16-byte tail: lane 0 below
                     if (en > st) {
@@ -1445,15 +1449,20 @@ int32_t dwt2_forward_host(const dwt2_plan *p, const float *host_in, float *host_
         if (cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
             cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking) != cudaSuccess)
             return fail(DWT2_ECUDA);
-        for (int i = 0; i < 64; ++i)
+        for (int i = 0; i < 132; ++i)
             if (cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming) != cudaSuccess) return fail(DWT2_ECUDA);
     }
     // Pipeline over NB row bands of level 1: H2D(band b) -> kernel on the
     // quad rows whose inputs have all arrived -> D2H of finished output rows.
     const LevelGeom &g = p->geom[0];
-    const int NB = std::min(16, std::max(1, g.Hq / 64));
+    static const int max_bands = [] {
+        const char *v = getenv("DWT2_HOST_BANDS");        // tuning override
+        const int n = v ? atoi(v) : 0;
+        return (n >= 1 && n <= 64) ? n : 32;
+    }();
+    const int NB = std::min(max_bands, std::max(1, g.Hq / 64));
     const size_t rowb = size_t(p->W) * sizeof(float);
-    cudaEvent_t *ev_in = p->ev, *ev_k = p->ev + 16, *ev_done = p->ev + 32;
+    cudaEvent_t *ev_in = p->ev, *ev_k = p->ev + 64, *ev_done = p->ev + 128;
     if (cudaEventRecord(ev_done[0], s) != cudaSuccess) return fail(DWT2_ECUDA);   // order after prior work
     if (cudaStreamWaitEvent(p->s_h2d, ev_done[0], 0) != cudaSuccess) return fail(DWT2_ECUDA);
     int q_done = 0;
@@ -1522,7 +1531,7 @@ void dwt2_destroy(dwt2_plan *p)
         cudaFree(p->d_out);
         cudaStreamDestroy(p->s_h2d);
         cudaStreamDestroy(p->s_d2h);
-        for (int i = 0; i < 64; ++i) cudaEventDestroy(p->ev[i]);
+        for (int i = 0; i < 132; ++i) cudaEventDestroy(p->ev[i]);
     }
     cudaGetLastError();
     delete p;

@@ -75,13 +75,17 @@ struct dwt2_plan {
     // host e2e staging
     mutable float *d_in, *d_out;
     mutable cudaStream_t s_h2d, s_d2h;
-    mutable cudaEvent_t ev[64];
+    mutable cudaEvent_t ev[132];      // host e2e: 64 band-arrived, 64 band-done, 4 sync
 };
 
 namespace dwt2_detail {
 
 // true if ptr is device (or managed) memory of the plan's device (cached)
 bool on_plan_device(const dwt2_plan *p, const void *ptr);
+
+// inverse of all levels through the K = 2 lifting kernel (dwt97.cu)
+int32_t run_inverse_k2(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,
+                       long long out_stride, cudaStream_t s);
 
 // all levels through the K = 2 lifting kernel (dwt97.cu)
 int32_t run_levels_k2(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,

@@ -448,6 +448,242 @@ int32_t launch_k2_level(const dwt2_plan *p, K2Args a, cudaStream_t s)
     return DWT2_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Inverse of the K = 2 kernel (9/7 and general lifting wavelets): undo the
+// scaling, then the four spatial steps in reverse (update 2, predict 2,
+// update 1, predict 1), each Eq. (5) factor inverted by negating its
+// polynomials.  Per quad row n loaded (after scaling: a2 = LL K^2, HL, LH,
+// hh2 = HH / K^2):
+//   undo U2, row n:    LH'2 = LH - c3 (hh2 + hh2[m-1]),  HL'2 = HL - c3 (hh2 + hh2[n-1]),
+//                      LL1  = a2 - c3 (HL'2 + HL'2[m-1]) - c3 (LH + LH[n-1])
+//   undo P2, row n-1:  HL1 = HL'2 - c2 (LL1 + LL1[m+1]),  LH1 = LH'2 - c2 (LL1 + LL1[n+1]),
+//                      HH1 = hh2 - c2 (LH1 + LH1[m+1]) - c2 (HL'2 + HL'2[n+1])
+//   undo U1, row n-1:  LH'1 = LH1 - c1 (HH1 + HH1[m-1]),  HL'1 = HL1 - c1 (HH1 + HH1[n-1]),
+//                      a    = LL1 - c1 (HL'1 + HL'1[m-1]) - c1 (LH1 + LH1[n-1])
+//   undo P1, row n-2:  b = HL'1 - c0 (a + a[m+1]),  c = LH'1 - c0 (a + a[n+1]),
+//                      d = HH1 - c0 (c + c[m+1]) - c0 (HL'1 + HL'1[n+1])
+// and pixel rows 2(n-2), 2(n-2)+1 are stored.  Boundaries: the coefficient
+// field of a whole-sample-symmetric input is itself symmetric in the
+// interleaved (pixel) index, so coefficients are fetched at mirrored pixel
+// positions (a coefficient of parity p at quad q sits at pixel 2q + p), the
+// same rule as the oracle's inverse (oracle/dwt97_oracle.c).
+// ---------------------------------------------------------------------------
+struct K2InvArgs {
+    const float *ll, *hl, *lh, *hh;        // plane origins of image 0
+    long long ll_pitch, ll_img, d_pitch, d_img;
+    float *out;                            // reconstructed level input
+    long long out_pitch, out_img;
+    int W, H;
+    int nslabs, tb, nblk, count;
+    long long ntiles;
+    double c0, c1, c2, c3, K2sq;           // K2sq = K^2
+};
+
+struct InvCarry {
+    double hh2, lh, hl2p, lh2p, ll1;        // row n-1: scaled HH, input LH, HL'2, LH'2, LL1
+    double hh1, lh1, a, hl1p, lh1p;         // row n-2: HH1, LH1, a, HL'1, LH'1
+};
+
+__device__ __forceinline__ int mqi(int q, int par, int n) { return (wssi(2 * q + par, n) - par) >> 1; }
+
+template <bool EDGE>
+__device__ __forceinline__ void kinv_load(const K2InvArgs &a, int img, int n, int m0, int lane, double (&LL)[2],
+                                          double (&HL)[2], double (&LH)[2], double (&HH)[2])
+{
+    const int nL = mqi(n, 0, a.H), nH = mqi(n, 1, a.H);
+    const float *pll = a.ll + (long long)img * a.ll_img + (long long)nL * a.ll_pitch;
+    const float *phl = a.hl + (long long)img * a.d_img + (long long)nL * a.d_pitch;
+    const float *plh = a.lh + (long long)img * a.d_img + (long long)nH * a.d_pitch;
+    const float *phh = a.hh + (long long)img * a.d_img + (long long)nH * a.d_pitch;
+    const int m = m0 - 2 + 2 * lane;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int mL = EDGE ? mqi(m + i, 0, a.W) : m + i;
+        const int mH = EDGE ? mqi(m + i, 1, a.W) : m + i;
+        LL[i] = (double)__ldg(pll + mL);
+        LH[i] = (double)__ldg(plh + mL);
+        HL[i] = (double)__ldg(phl + mH);
+        HH[i] = (double)__ldg(phh + mH);
+    }
+}
+
+template <bool EDGE>
+__device__ void kinv_tile(const K2InvArgs &a, int img, int m0, int n0, int n1, int lane)
+{
+    InvCarry cy[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) cy[i] = InvCarry{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const int r_first = n0 - 2, r_last = n1 + 1;
+    const int mo = m0 + 2 * (lane - 1);
+    const bool out_lane = lane >= 1 && lane <= 30;
+    double nLL[2], nHL[2], nLH[2], nHH[2];
+    kinv_load<EDGE>(a, img, r_first, m0, lane, nLL, nHL, nLH, nHH);
+    for (int n = r_first; n <= r_last; ++n) {
+        double LL[2], HL[2], LH[2], HH[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            LL[i] = nLL[i]; HL[i] = nHL[i]; LH[i] = nLH[i]; HH[i] = nHH[i];
+        }
+        if (n < r_last) kinv_load<EDGE>(a, img, n + 1, m0, lane, nLL, nHL, nLH, nHH);   // prefetch
+        // ---- scaling undone, undo U2 at row n
+        double a2[2], hh2[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            a2[i] = LL[i] * a.K2sq;
+            hh2[i] = HH[i] / a.K2sq;
+        }
+        const double hh2_l = shl(hh2[1]);
+        double lh2p[2], hl2p[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            lh2p[i] = fma(-a.c3, hh2[i] + (i == 0 ? hh2_l : hh2[0]), LH[i]);
+            hl2p[i] = fma(-a.c3, hh2[i] + cy[i].hh2, HL[i]);
+        }
+        const double hl2p_l = shl(hl2p[1]);
+        double ll1[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+            ll1[i] = fma(-a.c3, LH[i] + cy[i].lh, fma(-a.c3, hl2p[i] + (i == 0 ? hl2p_l : hl2p[0]), a2[i]));
+        // ---- undo P2 completes row n-1 (carried hl2p, lh2p, ll1, hh2 of row n-1)
+        double pll1[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) pll1[i] = cy[i].ll1;
+        const double ll1_r = shr(pll1[0]);
+        double hl1[2], lh1[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            hl1[i] = fma(-a.c2, pll1[i] + (i == 0 ? pll1[1] : ll1_r), cy[i].hl2p);
+            lh1[i] = fma(-a.c2, pll1[i] + ll1[i], cy[i].lh2p);
+        }
+        const double lh1_r = shr(lh1[0]);
+        double hh1[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+            hh1[i] = fma(-a.c2, cy[i].hl2p + hl2p[i], fma(-a.c2, lh1[i] + (i == 0 ? lh1[1] : lh1_r), cy[i].hh2));
+        // ---- undo U1, row n-1 (carried hh1, lh1 of row n-2)
+        const double hh1_l = shl(hh1[1]);
+        double lh1p[2], hl1p[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            lh1p[i] = fma(-a.c1, hh1[i] + (i == 0 ? hh1_l : hh1[0]), lh1[i]);
+            hl1p[i] = fma(-a.c1, hh1[i] + cy[i].hh1, hl1[i]);
+        }
+        const double hl1p_l = shl(hl1p[1]);
+        double av[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+            av[i] = fma(-a.c1, lh1[i] + cy[i].lh1, fma(-a.c1, hl1p[i] + (i == 0 ? hl1p_l : hl1p[0]), pll1[i]));
+        // ---- undo P1 completes row n-2 (carried a, hl1p, lh1p, hh1 of row n-2)
+        double pa[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) pa[i] = cy[i].a;
+        const double a_r = shr(pa[0]);
+        double bo[2], co[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            bo[i] = fma(-a.c0, pa[i] + (i == 0 ? pa[1] : a_r), cy[i].hl1p);
+            co[i] = fma(-a.c0, pa[i] + av[i], cy[i].lh1p);
+        }
+        const double c_r = shr(co[0]);
+        double dout[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+            dout[i] = fma(-a.c0, cy[i].hl1p + hl1p[i], fma(-a.c0, co[i] + (i == 0 ? co[1] : c_r), cy[i].hh1));
+        // ---- store pixel rows 2(n-2), 2(n-2)+1
+        const int q = n - 2;
+        if (q >= n0 && q < n1 && out_lane) {
+            const int x = 2 * mo, y = 2 * q;
+            float *r0 = a.out + (long long)img * a.out_img + (long long)y * a.out_pitch + x;
+            float *r1 = r0 + a.out_pitch;
+            const float e[4] = {(float)pa[0], (float)bo[0], (float)pa[1], (float)bo[1]};
+            const float o[4] = {(float)co[0], (float)dout[0], (float)co[1], (float)dout[1]};
+            const bool odd = y + 1 < a.H;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (x + j < a.W) {
+                    __stcs(r0 + j, e[j]);
+                    if (odd) __stcs(r1 + j, o[j]);
+                }
+            }
+        }
+        // ---- carries
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            cy[i].hh1 = hh1[i];
+            cy[i].lh1 = lh1[i];
+            cy[i].a = av[i];
+            cy[i].hl1p = hl1p[i];
+            cy[i].lh1p = lh1p[i];
+            cy[i].hh2 = hh2[i];
+            cy[i].lh = LH[i];
+            cy[i].hl2p = hl2p[i];
+            cy[i].lh2p = lh2p[i];
+            cy[i].ll1 = ll1[i];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(KT, 4) dwt_k2_inverse_kernel(const __grid_constant__ K2InvArgs a)
+{
+    pdl_launch97();
+    pdl_wait97();
+    const int lane = threadIdx.x & 31;
+    const long long nwarps = (long long)gridDim.x * KW;
+    const int Wq = (a.W + 1) >> 1, Hq = (a.H + 1) >> 1;
+    const long long per_img = (long long)a.nblk * a.nslabs;
+    for (long long t = (long long)blockIdx.x * KW + (threadIdx.x >> 5); t < a.ntiles; t += nwarps) {
+        const int img = int(t / per_img);
+        const int rr = int(t - img * per_img);
+        const int blk = rr / a.nslabs;
+        const int slab = rr - blk * a.nslabs;
+        const int m0 = slab * OUTQ;
+        const int n0 = blk * a.tb, n1 = min(n0 + a.tb, Hq);
+        // coefficient columns m0 - 2 .. m0 + 61 must exist in every plane for the unmirrored path
+        const bool edge = (m0 < 2) || (m0 + 62 > (a.W >> 1)) || (m0 + OUTQ > Wq);
+        if (edge) kinv_tile<true>(a, img, m0, n0, n1, lane);
+        else kinv_tile<false>(a, img, m0, n0, n1, lane);
+    }
+}
+
+int32_t launch_k2_inverse_level(const dwt2_plan *p, K2InvArgs a, cudaStream_t s)
+{
+    static int per_sm = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int n = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dwt_k2_inverse_kernel, KT, 0) != cudaSuccess || n < 1)
+            n = 1;
+        per_sm = n;
+    });
+    cudaGetLastError();
+    const int Wq = (a.W + 1) / 2, Hq = (a.H + 1) / 2;
+    a.nslabs = (Wq + OUTQ - 1) / OUTQ;
+    const long long warps = (long long)p->sms * per_sm * KW;
+    const long long slab_rows = (long long)a.count * a.nslabs * Hq;
+    long long tb = slab_rows / (4 * warps);
+    tb = std::max<long long>(16, std::min<long long>(512, tb));
+    a.tb = int(tb);
+    a.nblk = int((Hq + tb - 1) / tb);
+    a.ntiles = (long long)a.count * a.nblk * a.nslabs;
+    const long long want = (a.ntiles + KW - 1) / KW;
+    const int grid = int(std::max<long long>(1, std::min<long long>(want, warps / KW)));
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(KT);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, dwt_k2_inverse_kernel, a) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DWT2_ECUDA);
+    }
+    return DWT2_OK;
+}
+
 }  // namespace
 
 namespace dwt2_detail {
@@ -495,6 +731,52 @@ int32_t run_levels_k2(const dwt2_plan *p, const float *in, float *out, int count
             a.ll_img = p->sc_img_stride[si];
         }
         int32_t r = launch_k2_level(p, a, s);
+        if (r != DWT2_OK) return r;
+    }
+    return DWT2_OK;
+}
+
+// Inverse of all levels through the K = 2 kernel, coarsest first; buffer
+// roles as run_inverse in inverse.cu.
+int32_t run_inverse_k2(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,
+                       long long out_stride, cudaStream_t s)
+{
+    const Wavelet2 wv = wavelet_params(p);
+    for (int k = p->levels - 1; k >= 0; --k) {
+        const LevelGeom &g = p->geom[k];
+        K2InvArgs a;
+        memset(&a, 0, sizeof(a));
+        a.W = g.W;
+        a.H = g.H;
+        a.count = count;
+        a.c0 = wv.c0; a.c1 = wv.c1; a.c2 = wv.c2; a.c3 = wv.c3;
+        a.K2sq = wv.K * wv.K;
+        a.hl = in + g.Wq;
+        a.lh = in + (long long)g.Hq * p->W;
+        a.hh = a.lh + g.Wq;
+        a.d_pitch = p->W;
+        a.d_img = in_stride;
+        if (k == p->levels - 1) {
+            a.ll = in;
+            a.ll_pitch = p->W;
+            a.ll_img = in_stride;
+        } else {
+            const int si = k % 2;
+            a.ll = p->scratch[si];
+            a.ll_pitch = p->sc_pitch[si];
+            a.ll_img = p->sc_img_stride[si];
+        }
+        if (k == 0) {
+            a.out = out;
+            a.out_pitch = p->W;
+            a.out_img = out_stride;
+        } else {
+            const int si = (k - 1) % 2;
+            a.out = p->scratch[si];
+            a.out_pitch = p->sc_pitch[si];
+            a.out_img = p->sc_img_stride[si];
+        }
+        int32_t r = launch_k2_inverse_level(p, a, s);
         if (r != DWT2_OK) return r;
     }
     return DWT2_OK;

@@ -599,12 +599,13 @@ extern "C" {
 int32_t dwt2_inverse(const dwt2_plan *p, const float *in, float *out, dwt2_stream_t stream)
 {
     if (!p || !in || !out || p->strip || !aligned(in, 4) || !aligned(out, 4)) return fail(DWT2_EINVAL);
-    if (p->wavelet != DWT2_WAVELET_CDF53) return fail(DWT2_EUNSUPPORTED);
     const size_t bytes = size_t(p->W) * p->H * sizeof(float);
     if (overlap(in, bytes, out, bytes) || !on_plan_device(p, in) || !on_plan_device(p, out))
         return fail(DWT2_EINVAL);
     const long long img = (long long)p->W * p->H;
-    int32_t r = run_inverse(p, in, out, 1, img, img, reinterpret_cast<cudaStream_t>(stream));
+    int32_t r = p->wavelet != DWT2_WAVELET_CDF53
+                    ? run_inverse_k2(p, in, out, 1, img, img, reinterpret_cast<cudaStream_t>(stream))
+                    : run_inverse(p, in, out, 1, img, img, reinterpret_cast<cudaStream_t>(stream));
     if (r != DWT2_OK) return r;
     g_last_error = DWT2_OK;
     return DWT2_OK;
@@ -617,12 +618,13 @@ int32_t dwt2_inverse_batched(const dwt2_plan *p, const float *in, float *out, in
     if (!p || !in || !out || p->strip || count < 1 || count > p->max_count || in_stride < img ||
         out_stride < img || !aligned(in, 4) || !aligned(out, 4))
         return fail(DWT2_EINVAL);
-    if (p->wavelet != DWT2_WAVELET_CDF53) return fail(DWT2_EUNSUPPORTED);
     const size_t in_bytes = size_t((count - 1) * in_stride + img) * sizeof(float);
     const size_t out_bytes = size_t((count - 1) * out_stride + img) * sizeof(float);
     if (overlap(in, in_bytes, out, out_bytes) || !on_plan_device(p, in) || !on_plan_device(p, out))
         return fail(DWT2_EINVAL);
-    int32_t r = run_inverse(p, in, out, count, in_stride, out_stride, reinterpret_cast<cudaStream_t>(stream));
+    int32_t r = p->wavelet != DWT2_WAVELET_CDF53
+                    ? run_inverse_k2(p, in, out, count, in_stride, out_stride, reinterpret_cast<cudaStream_t>(stream))
+                    : run_inverse(p, in, out, count, in_stride, out_stride, reinterpret_cast<cudaStream_t>(stream));
     if (r != DWT2_OK) return r;
     g_last_error = DWT2_OK;
     return DWT2_OK;
