@@ -496,7 +496,7 @@ def main():
     k_bytes = runner.level1_bytes
     achieved = k_bytes / (k_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
-    traffic = ncu_traffic(cfg.name) if world == 1 else None
+    traffic = ncu_traffic(cfg.name if args.wavelet == "cdf53" else f"{cfg.name}_{args.wavelet}") if world == 1 else None
 
     # end to end through the host-buffer API
     e2e = None
