@@ -289,10 +289,8 @@ __device__ __forceinline__ void icp_wait() { asm volatile("cp.async.wait_group %
 // update per chunk.
 struct ChunkPlan {
     const float *src[3];        // chunk address at row 0 (image and column applied)
-    long long pitch[3];
     int dst[3];                 // float offset in the stage
-    bool lh_hh[3];              // rows clamped to the LH / HH range
-    const float *lo[3], *hi[3]; // allocation range (zero fill outside)
+    int pl[3];                  // plane: 0 LL, 1 HL, 2 LH, 3 HH
 };
 
 __device__ __forceinline__ ChunkPlan chunk_plan(const InvArgs &a, int img, int m0, int lane)
@@ -305,25 +303,30 @@ __device__ __forceinline__ ChunkPlan chunk_plan(const InvArgs &a, int img, int m
         const float *base = pl == 0 ? a.ll : pl == 1 ? a.hl : pl == 2 ? a.lh : a.hh;
         const long long img_off = (long long)img * (pl == 0 ? a.ll_img : a.d_img);
         P.src[t] = base + img_off + (m0 - 4 + 4 * k);
-        P.pitch[t] = pl == 0 ? a.ll_pitch : a.d_pitch;
         P.dst[t] = pl * IWIN + 4 * k;
-        P.lh_hh[t] = pl >= 2;
-        P.lo[t] = pl == 0 ? a.ll_lo : a.d_lo;
-        P.hi[t] = pl == 0 ? a.ll_hi : a.d_hi;
+        P.pl[t] = pl;
     }
     return P;
 }
 
-// issue the 72 chunks of quad row n (4 planes x 18) into stage `st`
+// issue the 72 chunks of quad row n (4 planes x 18) into stage `st`.  Only
+// edge slabs (first / last) can reach outside the buffers (columns left of
+// plane 0 or past the last row's end): interior slabs skip the range check.
+template <bool EDGE>
 __device__ __forceinline__ void ring_issue(const InvArgs &a, const ChunkPlan &P, float *st, int n, int lane)
 {
     const int nd = min(max(n, 0), (a.H >> 1) - 1);
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
         if (t < 2 || lane < 8) {
-            const float *src = P.src[t] + (long long)(P.lh_hh[t] ? nd : n) * P.pitch[t];
-            const uint32_t nb = (src >= P.lo[t] && src + 4 <= P.hi[t]) ? 16u : 0u;   // outside: zero fill
-            icp_async16(st + P.dst[t], nb ? src : P.lo[t], nb);
+            const float *src = P.src[t] + (long long)(P.pl[t] >= 2 ? nd : n) * (P.pl[t] == 0 ? a.ll_pitch : a.d_pitch);
+            if (EDGE) {
+                const float *lo = P.pl[t] == 0 ? a.ll_lo : a.d_lo, *hi = P.pl[t] == 0 ? a.ll_hi : a.d_hi;
+                const uint32_t nb = (src >= lo && src + 4 <= hi) ? 16u : 0u;   // outside: zero fill
+                icp_async16(st + P.dst[t], nb ? src : lo, nb);
+            } else {
+                icp_async16(st + P.dst[t], src, 16u);
+            }
         }
     }
 }
@@ -379,7 +382,7 @@ __device__ __forceinline__ void ring_tile(const InvArgs &a, float *ring, int img
     auto row_of = [&](int i) { return i == 0 ? max(n0 - 1, 0) : n0 + i - 1; };
 #pragma unroll
     for (int j = 0; j < IDS; ++j) {
-        if (j < T) ring_issue(a, P, ring + j * ISTAGE, row_of(j), lane);
+        if (j < T) ring_issue<EDGE>(a, P, ring + j * ISTAGE, row_of(j), lane);
         icp_commit();
     }
     Rec prev;
@@ -406,7 +409,7 @@ __device__ __forceinline__ void ring_tile(const InvArgs &a, float *ring, int img
                 prev = rc;
             }
             // the stage's values are in registers (used above): refill it
-            if (i + IDS < T) ring_issue(a, P, ring + j * ISTAGE, row_of(i + IDS), lane);
+            if (i + IDS < T) ring_issue<EDGE>(a, P, ring + j * ISTAGE, row_of(i + IDS), lane);
             icp_commit();
         }
     }
@@ -431,7 +434,10 @@ __global__ void __launch_bounds__(IRW * 32, 3) dwt53_inverse_ring_kernel(const _
         const int slab = r - blk * a.nslabs;
         const int m0 = slab * IQ;
         const int n0 = blk * a.tb, n1 = min(n0 + a.tb, Hq);
-        if ((m0 == 0) || (m0 + IQ >= Wq)) ring_tile<true>(a, ring, img, m0, n0, n1, lane);
+        // interior: every plane's window [m0 - 4, m0 + 68) lies inside its row
+        // (the narrowest planes, HL / HH, are Wh wide), so no clamping and no
+        // range check of the cp.async sources
+        if ((m0 == 0) || (m0 + IWIN - 4 > (a.W >> 1))) ring_tile<true>(a, ring, img, m0, n0, n1, lane);
         else ring_tile<false>(a, ring, img, m0, n0, n1, lane);
     }
 }
