@@ -1,3 +1,4 @@
+# Test tooling (runs the oracle), kept under tests/ (not collected: no test_ prefix).
 """Locate parity failures: for each (W, H, L) print max error per level/band."""
 import sys
 import numpy as np
