@@ -37,7 +37,41 @@ sys.path.insert(0, ROOT)
 METRIC = "forward 2-D CDF 5/3 DWT Gpixel/s and HBM GB/s vs peak, 1/2/4/8 B200"
 UNIT = "Gpixel/s"
 BYTES_PER_PX = 8            # algorithmic: 4 B read + 4 B written per pixel per level
+# algorithmic bytes per pixel per level of the comparison schemes (each step one HBM pass; the in-place
+# separable steps 2-4 read 4 B and write 2 B): see scripts/scheme_compare.py, DESIGN.md 5.3
+SCHEME_BYTES = {"fused": 8, "nonsep_naive": 8, "nonsep_lifting": 16, "nonsep_adapted": 16, "sep_conv": 16,
+                "sep_lifting": 26}
+SCHEME_STEPS = {"fused": 1, "nonsep_naive": 1, "nonsep_lifting": 2, "nonsep_adapted": 2, "sep_conv": 2,
+                "sep_lifting": 4}
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def config_dict(args, cfg, world):
+    d = describe(cfg, world)
+    if args.wavelet != "cdf53":
+        d["wavelet"] = args.wavelet
+    if args.op != "forward":
+        d["op"] = args.op
+    if args.scheme != "fused":
+        d["scheme"] = args.scheme
+    return d
+
+
+def kernel_label(args):
+    if args.scheme != "fused":
+        return f"{args.scheme} scheme kernels ({SCHEME_STEPS[args.scheme]} per level)"
+    if args.op == "inverse":
+        return "dwt53_inverse kernel" if args.wavelet == "cdf53" else "dwt_k2_inverse_kernel"
+    return "dwt53_level_kernel" if args.wavelet == "cdf53" else "dwt_k2_level_kernel"
+
+
+def metric_name(args):
+    m = METRIC if args.wavelet == "cdf53" else METRIC.replace("CDF 5/3", "CDF 9/7")
+    if args.op == "inverse":
+        m = m.replace("forward", "inverse", 1)
+    if args.scheme != "fused":
+        m = m.replace("DWT", f"DWT ({args.scheme} scheme, one kernel per step)", 1)
+    return m
 
 
 def parse():
@@ -47,6 +81,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="3", choices=["1", "2", "3", "4", "4b", "5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--op", default="forward", choices=["forward", "inverse"],
+                    help="inverse: time the inverse transform (SURVEY 8f N2) of the config's pyramid")
+    ap.add_argument("--scheme", default="fused", choices=["fused", "nonsep_naive", "nonsep_lifting", "nonsep_adapted",
+                                                        "sep_conv", "sep_lifting"],
+                    help="forward with one of the paper's schemes, one kernel per step (SURVEY 8f N1)")
     ap.add_argument("--wavelet", default="cdf53", choices=["cdf53", "cdf97"],
                     help="cdf97: the K = 2 non-separable kernel (SURVEY 8f N4); single-image and batch configs")
     ap.add_argument("--no-overlap", action="store_true", help="strips: exchange, then one launch")
@@ -180,23 +219,27 @@ class OursRunner:
                 out = torch.empty_like(x)
                 plan = dwt2.Plan(grp.width, grp.height, cfg.levels, max_count=len(idx), wavelet=self.wavelet)
                 info = plan.info()
+                if self.op == "inverse":
+                    x = plan.forward(x).clone()          # the pyramid is the inverse's input
                 self.items.append((plan, x, out))
-                self.launches += info.launches_per_forward
-                self.algo_bytes += info.algorithmic_bytes * len(idx)
-                self.level1_bytes += BYTES_PER_PX * grp.width * grp.height * len(idx)
+                self.launches += info.launches_per_forward * SCHEME_STEPS[self.scheme]
+                self.algo_bytes += info.algorithmic_bytes * len(idx) * SCHEME_BYTES[self.scheme] // BYTES_PER_PX
+                self.level1_bytes += SCHEME_BYTES[self.scheme] * grp.width * grp.height * len(idx)
                 self.pixels += grp.width * grp.height * len(idx)
             self.mode = "batch"
         elif world == 1:
             g = cfg.groups[0]
             x = torch.from_numpy(g.image(0)).to(device)
+            self.plan = dwt2.Plan(g.width, g.height, cfg.levels, wavelet=self.wavelet)
+            if self.op == "inverse":
+                x = self.plan.forward(x).clone()           # the pyramid is the inverse's input
             self.xs = [x] + [x.clone() for _ in range(self.nbuf - 1)]
             self.outs = [torch.empty_like(x) for _ in range(self.nbuf)]
             self.x, self.out = x, self.outs[0]
-            self.plan = dwt2.Plan(g.width, g.height, cfg.levels, wavelet=self.wavelet)
             info = self.plan.info()
-            self.launches = info.launches_per_forward
-            self.algo_bytes = info.algorithmic_bytes
-            self.level1_bytes = BYTES_PER_PX * g.width * g.height
+            self.launches = info.launches_per_forward * SCHEME_STEPS[self.scheme]
+            self.algo_bytes = info.algorithmic_bytes * SCHEME_BYTES[self.scheme] // BYTES_PER_PX
+            self.level1_bytes = SCHEME_BYTES[self.scheme] * g.width * g.height
             self.pixels = g.width * g.height
             self.mode = "single"
             self.host_img = g.image(0)
@@ -219,6 +262,17 @@ class OursRunner:
     overlap_off = False
     wavelet = "cdf53"
     steps = 20
+    op = "forward"
+    scheme = "fused"
+
+    def call(self, plan, x, out):
+        """The timed operation on one buffer pair."""
+        if self.op == "inverse":
+            plan.inverse(x, out)
+        elif self.scheme != "fused":
+            plan.forward_scheme(self.scheme, x, out)
+        else:
+            plan.forward(x, out)
 
     def flush_l2(self):
         """Evict the L2 with clean lines: a read-only pass over 256 MB (a
@@ -231,10 +285,10 @@ class OursRunner:
         if self.mode == "single":
             j = self.i % self.nbuf
             self.i += 1
-            self.plan.forward(self.xs[j], self.outs[j])
+            self.call(self.plan, self.xs[j], self.outs[j])
         elif self.mode == "batch":
             for plan, x, out in self.items:
-                plan.forward(x, out)
+                self.call(plan, x, out)
         else:
             self.D.strip_pyramid_step(self.ex, self.splan, overlap=not self.overlap_off)
 
@@ -255,7 +309,7 @@ class OursRunner:
             plans = [(self.dwt2.Plan(p.width, p.height, 1, max_count=x.shape[0], wavelet=self.wavelet), x, o)
                      for p, x, o in self.items]
         for p, x, o in plans:          # warm-up (tensor maps, first-launch costs)
-            p.forward(x, o)
+            self.call(p, x, o)
         torch.cuda.synchronize()
         # back to back between one event pair (event ticks are 2.048 us);
         # with a flush, K flushes timed alone are subtracted
@@ -264,7 +318,7 @@ class OursRunner:
         for _ in range(iters):
             self.flush_l2()
             for p, x, o in plans:
-                p.forward(x, o)
+                self.call(p, x, o)
         e1.record(s)
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(s)
@@ -281,6 +335,27 @@ class OursRunner:
         step's input from pinned memory and D2H of its result are inside the
         timed region (the C-ABI dwt2_forward_host pipelines them by row band)."""
         torch = self.torch
+        if self.mode == "single" and (self.op != "forward" or self.scheme != "fused" or self.wavelet != "cdf53"):
+            # inverse / schemes / 9/7: H2D of the input, the operation, D2H of the result
+            hin = self.x.cpu().pin_memory()
+            hout = torch.empty_like(hin).pin_memory()
+            s = torch.cuda.current_stream()
+
+            def one():
+                self.x.copy_(hin, non_blocking=True)
+                self.call(self.plan, self.x, self.out)
+                hout.copy_(self.out, non_blocking=True)
+            for _ in range(warm):
+                one()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(steps):
+                one()
+            e1.record(s)
+            e1.synchronize()
+            self.h2d = self.d2h = hin.numel() * 4
+            return e0.elapsed_time(e1) / 1e3 / steps
         if self.mode == "single":
             hin = torch.from_numpy(self.host_img).pin_memory()
             hout = torch.empty_like(hin).pin_memory()
@@ -322,7 +397,7 @@ class OursRunner:
         def one():
             for (hi, ho), (plan, x, o) in zip(hosts, self.items):
                 x.copy_(hi, non_blocking=True)
-                plan.forward(x, o)
+                self.call(plan, x, o)
                 ho.copy_(o, non_blocking=True)
         for _ in range(warm):
             one()
@@ -338,7 +413,7 @@ class OursRunner:
         return e0.elapsed_time(e1) / 1e3 / steps
 
 
-def oracle_sample(cfg, budget_s: float, rows: int = 0, wavelet: str = "cdf53"):
+def oracle_sample(cfg, budget_s: float, rows: int = 0, wavelet: str = "cdf53", op: str = "forward"):
     """Bounded sample of the workload for the CPU oracle: a full-width band of
     the first image (or whole images for config 5), transformed as a
     standalone image with the config's levels.  Returns (fn, pixels, text)."""
@@ -363,6 +438,15 @@ def oracle_sample(cfg, budget_s: float, rows: int = 0, wavelet: str = "cdf53"):
         w, h, L = g.width, rows, 0
         while L < lv and w >= 2 and h >= 2:
             w, h, L = (w + 1) // 2, (h + 1) // 2, L + 1
+
+    if op == "inverse":
+        y64 = oracle.forward(x64, L, round_f32=True, wavelet=wavelet)      # the band's pyramid (untimed)
+
+        def fn():
+            oracle.inverse(y64, L, round_f32=True, wavelet=wavelet)
+        alg = "C97 (9/7 inverse lifting" if wavelet == "cdf97" else "C (inverse lifting"
+        return fn, g.width * rows, (f"{g.width}x{rows} band of image 0 of config {cfg.name}, {L} level(s), "
+                                    f"oracle algorithm {alg}, fp64), 1 thread")
 
     def fn():
         oracle.forward(x64, L, round_f32=True, wavelet=wavelet)
@@ -396,7 +480,7 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     per_step_budget = 0.5
-    fn, px, text = oracle_sample(cfg, per_step_budget, args.cpu_sample_rows, args.wavelet)
+    fn, px, text = oracle_sample(cfg, per_step_budget, args.cpu_sample_rows, args.wavelet, args.op)
     for _ in range(args.warmup):
         fn()
     t0 = time.perf_counter()
@@ -404,11 +488,10 @@ def run_reference(args, cfg):
         fn()
     dt = (time.perf_counter() - t0) / args.steps
     v = px / dt / 1e9
-    metric = METRIC if args.wavelet == "cdf53" else METRIC.replace("CDF 5/3", "CDF 9/7")
-    line = {"impl": "reference", "metric": metric, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": metric_name(args), "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "strong" if cfg.name != "5" else "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": describe(cfg, 1),
+            "data": "synthetic", "config": config_dict(args, cfg, 1),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": text},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -434,6 +517,12 @@ def main():
 
     OursRunner.overlap_off = args.no_overlap
     OursRunner.steps = args.steps
+    OursRunner.op = args.op
+    OursRunner.scheme = args.scheme
+    if (args.op != "forward" or args.scheme != "fused") and world > 1 and cfg.name != "5":
+        raise SystemExit("row strips run the forward fused kernel only")
+    if args.scheme != "fused" and (args.op != "forward" or args.wavelet != "cdf53"):
+        raise SystemExit("the comparison schemes are forward CDF 5/3")
     OursRunner.wavelet = args.wavelet
     if args.wavelet != "cdf53" and world > 1 and cfg.name != "5":
         raise SystemExit("row strips run the CDF 5/3 kernel only")
@@ -492,11 +581,13 @@ def main():
     # dominant kernel (level 1) duration
     k_ms = runner.level1_kernel_ms(max(3, args.steps))
     if k_ms is None:
-        k_ms = ms / max(1, (runner.launches if runner.mode != "strip" else 1))
+        # one-level configs: the level (all its step kernels for a scheme) is the step
+        k_ms = ms / max(1, (runner.launches // SCHEME_STEPS[args.scheme] if runner.mode != "strip" else 1))
     k_bytes = runner.level1_bytes
     achieved = k_bytes / (k_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
-    traffic = ncu_traffic(cfg.name if args.wavelet == "cdf53" else f"{cfg.name}_{args.wavelet}") if world == 1 else None
+    traffic = ncu_traffic(cfg.name if args.wavelet == "cdf53" else f"{cfg.name}_{args.wavelet}") \
+        if world == 1 and args.op == "forward" and args.scheme == "fused" else None
 
     # end to end through the host-buffer API
     e2e = None
@@ -511,7 +602,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        fn, px, text = oracle_sample(cfg, 10.0, args.cpu_sample_rows, args.wavelet)
+        fn, px, text = oracle_sample(cfg, 10.0, args.cpu_sample_rows, args.wavelet, args.op)
         t0 = time.perf_counter()
         fn()
         dt = time.perf_counter() - t0
@@ -522,18 +613,17 @@ def main():
         algo_bytes_total = runner.algo_bytes * world if cfg.name != "5" else sum(
             BYTES_PER_PX * workloads.level_pixels(g.width, g.height, cfg.levels) * g.count for g in cfg.groups)
         line = {
-            "metric": METRIC if args.wavelet == "cdf53" else METRIC.replace("CDF 5/3", "CDF 9/7"),
+            "metric": metric_name(args),
             "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "weak" if cfg.name == "5" else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(describe(cfg, world), **({"wavelet": args.wavelet} if args.wavelet != "cdf53" else {})),
+            "config": config_dict(args, cfg, world),
             "hbm_gbs_algorithmic": algo_bytes_total / (ms_max * 1e-3) / 1e9,
             "ns_per_pel": ms_max * 1e6 / total_px,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("dwt53_level_kernel" if args.wavelet == "cdf53" else "dwt_k2_level_kernel")
-                         + " (level 1)", "kernel_ms": k_ms,
+                         "kernel": kernel_label(args) + " (level 1)", "kernel_ms": k_ms,
                          "bytes_per_launch": k_bytes, "peak_source": peak_src,
                          "frac_of_8tbs": achieved / 8000.0},
             "cpu_baseline": cpu,

@@ -476,7 +476,9 @@ struct K2InvArgs {
     int W, H;
     int nslabs, tb, nblk, count;
     long long ntiles;
-    double c0, c1, c2, c3, K2sq;           // K2sq = K^2
+    double c0, c1, c2, c3, K2sq, invK2sq;  // K^2 and 1 / K^2
+    int async;                             // 1: every plane 8-byte aligned with even pitches (cp.async ring)
+    int vec_out;                           // 1: output 16-byte aligned with pitch % 4 == 0 (float4 stores)
 };
 
 struct InvCarry {
@@ -486,9 +488,12 @@ struct InvCarry {
 
 __device__ __forceinline__ int mqi(int q, int par, int n) { return (wssi(2 * q + par, n) - par) >> 1; }
 
+struct InvRaw {
+    float LL[2], HL[2], LH[2], HH[2];
+};
+
 template <bool EDGE>
-__device__ __forceinline__ void kinv_load(const K2InvArgs &a, int img, int n, int m0, int lane, double (&LL)[2],
-                                          double (&HL)[2], double (&LH)[2], double (&HH)[2])
+__device__ __forceinline__ InvRaw kinv_load(const K2InvArgs &a, int img, int n, int m0, int lane)
 {
     const int nL = mqi(n, 0, a.H), nH = mqi(n, 1, a.H);
     const float *pll = a.ll + (long long)img * a.ll_img + (long long)nL * a.ll_pitch;
@@ -496,41 +501,89 @@ __device__ __forceinline__ void kinv_load(const K2InvArgs &a, int img, int n, in
     const float *plh = a.lh + (long long)img * a.d_img + (long long)nH * a.d_pitch;
     const float *phh = a.hh + (long long)img * a.d_img + (long long)nH * a.d_pitch;
     const int m = m0 - 2 + 2 * lane;
+    InvRaw R;
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
         const int mL = EDGE ? mqi(m + i, 0, a.W) : m + i;
         const int mH = EDGE ? mqi(m + i, 1, a.W) : m + i;
-        LL[i] = (double)__ldg(pll + mL);
-        LH[i] = (double)__ldg(plh + mL);
-        HL[i] = (double)__ldg(phl + mH);
-        HH[i] = (double)__ldg(phh + mH);
+        R.LL[i] = __ldg(pll + mL);
+        R.LH[i] = __ldg(plh + mL);
+        R.HL[i] = __ldg(phl + mH);
+        R.HH[i] = __ldg(phh + mH);
     }
+    return R;
 }
 
-template <bool EDGE>
-__device__ void kinv_tile(const K2InvArgs &a, int img, int m0, int n0, int n1, int lane)
+__device__ __forceinline__ void cp_async8(float *dst, const float *src)
 {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src) : "memory");
+}
+
+constexpr int IDSK = 8;                        // quad rows in flight per warp (inverse ring)
+constexpr size_t KINV_SMEM = size_t(KW) * IDSK * 4 * 64 * sizeof(float);
+
+// Interior slabs with 8-byte aligned planes stream their rows through a
+// per-warp shared-memory ring (cp.async, IDSK rows in flight); edge slabs
+// (mirrored columns) or unaligned planes load through registers.
+template <bool EDGE, bool ASYNC>
+__device__ void kinv_tile(const K2InvArgs &a, float *ring, int img, int m0, int n0, int n1, int lane)
+{
+    constexpr int D = ASYNC ? IDSK : 1;
     InvCarry cy[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) cy[i] = InvCarry{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     const int r_first = n0 - 2, r_last = n1 + 1;
     const int mo = m0 + 2 * (lane - 1);
     const bool out_lane = lane >= 1 && lane <= 30;
-    double nLL[2], nHL[2], nLH[2], nHH[2];
-    kinv_load<EDGE>(a, img, r_first, m0, lane, nLL, nHL, nLH, nHH);
-    for (int n = r_first; n <= r_last; ++n) {
+    InvRaw reg[ASYNC ? 1 : D];
+    auto issue = [&](int j, int n) {                 // j: compile-time slot
+        if (ASYNC) {
+            const int nL = mqi(n, 0, a.H), nH = mqi(n, 1, a.H);
+            const int m = m0 - 2 + 2 * lane;
+            float *st = ring + j * (4 * 64) + 2 * lane;
+            cp_async8(st, a.ll + (long long)img * a.ll_img + (long long)nL * a.ll_pitch + m);
+            cp_async8(st + 64, a.hl + (long long)img * a.d_img + (long long)nL * a.d_pitch + m);
+            cp_async8(st + 128, a.lh + (long long)img * a.d_img + (long long)nH * a.d_pitch + m);
+            cp_async8(st + 192, a.hh + (long long)img * a.d_img + (long long)nH * a.d_pitch + m);
+        } else {
+            reg[ASYNC ? 0 : j] = kinv_load<EDGE>(a, img, n, m0, lane);
+        }
+    };
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        issue(j, r_first + j);
+        if (ASYNC) cp_async_commit();
+    }
+    for (int rb = r_first; rb <= r_last; rb += D) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        const int n = rb + j;
+        InvRaw R;
+        if (ASYNC) {
+            cp_async_wait<D - 1>();
+            const float *st = ring + j * (4 * 64) + 2 * lane;
+            const float2 ll = *reinterpret_cast<const float2 *>(st);
+            const float2 hl = *reinterpret_cast<const float2 *>(st + 64);
+            const float2 lh = *reinterpret_cast<const float2 *>(st + 128);
+            const float2 hh = *reinterpret_cast<const float2 *>(st + 192);
+            R.LL[0] = ll.x; R.LL[1] = ll.y; R.HL[0] = hl.x; R.HL[1] = hl.y;
+            R.LH[0] = lh.x; R.LH[1] = lh.y; R.HH[0] = hh.x; R.HH[1] = hh.y;
+        } else {
+            R = reg[ASYNC ? 0 : j];
+            issue(j, n + D);
+        }
         double LL[2], HL[2], LH[2], HH[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            LL[i] = nLL[i]; HL[i] = nHL[i]; LH[i] = nLH[i]; HH[i] = nHH[i];
+            LL[i] = R.LL[i]; HL[i] = R.HL[i]; LH[i] = R.LH[i]; HH[i] = R.HH[i];
         }
-        if (n < r_last) kinv_load<EDGE>(a, img, n + 1, m0, lane, nLL, nHL, nLH, nHH);   // prefetch
         // ---- scaling undone, undo U2 at row n
         double a2[2], hh2[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             a2[i] = LL[i] * a.K2sq;
-            hh2[i] = HH[i] / a.K2sq;
+            hh2[i] = HH[i] * a.invK2sq;
         }
         const double hh2_l = shl(hh2[1]);
         double lh2p[2], hl2p[2];
@@ -598,11 +651,16 @@ __device__ void kinv_tile(const K2InvArgs &a, int img, int m0, int n0, int n1, i
             const float e[4] = {(float)pa[0], (float)bo[0], (float)pa[1], (float)bo[1]};
             const float o[4] = {(float)co[0], (float)dout[0], (float)co[1], (float)dout[1]};
             const bool odd = y + 1 < a.H;
+            if (!EDGE && a.vec_out) {
+                __stcs(reinterpret_cast<float4 *>(r0), make_float4(e[0], e[1], e[2], e[3]));
+                if (odd) __stcs(reinterpret_cast<float4 *>(r1), make_float4(o[0], o[1], o[2], o[3]));
+            } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (x + j < a.W) {
-                    __stcs(r0 + j, e[j]);
-                    if (odd) __stcs(r1 + j, o[j]);
+                for (int j = 0; j < 4; ++j) {
+                    if (x + j < a.W) {
+                        __stcs(r0 + j, e[j]);
+                        if (odd) __stcs(r1 + j, o[j]);
+                    }
                 }
             }
         }
@@ -620,14 +678,22 @@ __device__ void kinv_tile(const K2InvArgs &a, int img, int m0, int n0, int n1, i
             cy[i].lh2p = lh2p[i];
             cy[i].ll1 = ll1[i];
         }
+        if (ASYNC) {
+            if (rb + D <= r_last) issue(j, n + D);     // slot j's row was consumed above
+            cp_async_commit();
+        }
     }
+    }
+    if (ASYNC) cp_async_wait<0>();
 }
 
 __global__ void __launch_bounds__(KT, 4) dwt_k2_inverse_kernel(const __grid_constant__ K2InvArgs a)
 {
+    extern __shared__ __align__(16) float kinv_smem[];
     pdl_launch97();
     pdl_wait97();
     const int lane = threadIdx.x & 31;
+    float *ring = kinv_smem + (threadIdx.x >> 5) * (IDSK * 4 * 64);
     const long long nwarps = (long long)gridDim.x * KW;
     const int Wq = (a.W + 1) >> 1, Hq = (a.H + 1) >> 1;
     const long long per_img = (long long)a.nblk * a.nslabs;
@@ -640,8 +706,9 @@ __global__ void __launch_bounds__(KT, 4) dwt_k2_inverse_kernel(const __grid_cons
         const int n0 = blk * a.tb, n1 = min(n0 + a.tb, Hq);
         // coefficient columns m0 - 2 .. m0 + 61 must exist in every plane for the unmirrored path
         const bool edge = (m0 < 2) || (m0 + 62 > (a.W >> 1)) || (m0 + OUTQ > Wq);
-        if (edge) kinv_tile<true>(a, img, m0, n0, n1, lane);
-        else kinv_tile<false>(a, img, m0, n0, n1, lane);
+        if (edge) kinv_tile<true, false>(a, ring, img, m0, n0, n1, lane);
+        else if (a.async) kinv_tile<false, true>(a, ring, img, m0, n0, n1, lane);
+        else kinv_tile<false, false>(a, ring, img, m0, n0, n1, lane);
     }
 }
 
@@ -651,7 +718,10 @@ int32_t launch_k2_inverse_level(const dwt2_plan *p, K2InvArgs a, cudaStream_t s)
     static std::once_flag once;
     std::call_once(once, [] {
         int n = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dwt_k2_inverse_kernel, KT, 0) != cudaSuccess || n < 1)
+        if (cudaFuncSetAttribute(dwt_k2_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(KINV_SMEM)) !=
+                cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dwt_k2_inverse_kernel, KT, KINV_SMEM) != cudaSuccess ||
+            n < 1)
             n = 1;
         per_sm = n;
     });
@@ -671,12 +741,16 @@ int32_t launch_k2_inverse_level(const dwt2_plan *p, K2InvArgs a, cudaStream_t s)
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(KT);
+    cfg.dynamicSmemBytes = KINV_SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    a.async = aligned(a.ll, 8) && aligned(a.hl, 8) && aligned(a.lh, 8) && aligned(a.hh, 8) && a.ll_pitch % 2 == 0 &&
+              a.d_pitch % 2 == 0 && (a.count == 1 || (a.ll_img % 2 == 0 && a.d_img % 2 == 0)) ? 1 : 0;
+    a.vec_out = aligned(a.out, 16) && a.out_pitch % 4 == 0 && (a.count == 1 || a.out_img % 4 == 0) ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, dwt_k2_inverse_kernel, a) != cudaSuccess) {
         cudaGetLastError();
         return fail(DWT2_ECUDA);
@@ -751,6 +825,7 @@ int32_t run_inverse_k2(const dwt2_plan *p, const float *in, float *out, int coun
         a.count = count;
         a.c0 = wv.c0; a.c1 = wv.c1; a.c2 = wv.c2; a.c3 = wv.c3;
         a.K2sq = wv.K * wv.K;
+        a.invK2sq = 1.0 / (wv.K * wv.K);
         a.hl = in + g.Wq;
         a.lh = in + (long long)g.Hq * p->W;
         a.hh = a.lh + g.Wq;
