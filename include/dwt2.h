@@ -183,7 +183,10 @@ int32_t dwt2_forward_batched(const dwt2_plan *plan, const float *in, float *out,
 /* Forward transform of a one-level strip plan (see dwt2_plan_create_strip for the
  * `in` / `out` layouts).  part selects all quad rows, only the interior ones
  * (which read no ghost row, so they may run while the ghost rows are still in
- * flight) or only the two boundary quad rows. */
+ * flight) or only the two boundary quad rows.  A BOUNDARY call may run on
+ * another stream concurrently with the INTERIOR call of the same level (they
+ * write disjoint rows and use separate work queues); other calls on one plan
+ * must be serialised. */
 int32_t dwt2_forward_strip(const dwt2_plan *plan, const float *in, float *out, int32_t part,
                            dwt2_stream_t stream);
 

@@ -104,7 +104,8 @@ constexpr int WARPS = DWT2_WARPS;           // warps per CTA (independent; packi
 constexpr int THREADS = WARPS * 32;
 constexpr int MIN_TILE_ROWS = 11;           // min quad rows per tile (sweep: 11 > 7, 15 on 4096^2 and 8192^2)
 constexpr int MAX_TILE_ROWS = 127;
-constexpr int MAX_COUNTERS = MAX_LEVELS;    // levels with a work-queue counter pair
+constexpr int MAX_COUNTERS = 2 * MAX_LEVELS;  // work-queue counter pairs: per level, and per level for strip
+                                              // BOUNDARY launches (which may run concurrently with INTERIOR)
 
 // smem row pitch: TMA writes a box densely (136); the cp.async loader keeps
 // every row's 16-byte alignment shift delta (0..3 floats), hence 4 more.
@@ -879,7 +880,7 @@ const TilePolicy &tile_policy()
 }
 
 int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO &io, int qa0, int qa1, int qb0,
-                     int qb1, cudaStream_t stream)
+                     int qb1, cudaStream_t stream, int queue = 0)
 {
     LevelArgs a;
     memset(&a, 0, sizeof(a));
@@ -914,7 +915,7 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     const bool vec = aligned(a.ll, va) && aligned(a.hl, va) && aligned(a.lh, va) && aligned(a.hh, va) &&
                      io.ll_pitch % QPL == 0 && io.out_pitch % QPL == 0 &&
                      (io.count == 1 || (io.ll_img_stride % QPL == 0 && io.out_img_stride % QPL == 0));
-    if (level < 0 || level >= MAX_COUNTERS) return fail(DWT2_EINVAL);
+    if (level < 0 || level >= MAX_LEVELS) return fail(DWT2_EINVAL);
     dwt2_plan::TmapCache &tc = p->tcache[level];
     if (tma && tc.in == io.in && tc.pitch == io.in_pitch && tc.stride == io.in_img_stride && tc.W == W &&
         tc.rows == io.in_rows && tc.count == io.count) {
@@ -964,7 +965,7 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     const int grid = int(std::max<long long>(1, std::min<long long>(max_ctas, want_ctas)));
     a.nwarps = grid * WARPS;
     a.static_tiles = ntiles <= a.nwarps ? 1 : 0;
-    a.counter = p->counters + 2 * level;
+    a.counter = p->counters + 2 * (level + (queue ? MAX_LEVELS : 0));
 
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
@@ -1419,8 +1420,10 @@ int32_t dwt2_forward_strip_level(const dwt2_plan *p, int32_t level, const float 
         b0 = std::max(ib, ia); b1 = qe;
         if (b0 < a1) b0 = a1;
     }
+    // BOUNDARY launches use their own work-queue counters, so they may run on
+    // another stream concurrently with the INTERIOR launch of the same level
     int32_t r = launch_level(p, level, L.width, L.global_height, io, a0, a1, b0, b1,
-                             reinterpret_cast<cudaStream_t>(stream));
+                             reinterpret_cast<cudaStream_t>(stream), part == DWT2_STRIP_BOUNDARY ? 1 : 0);
     if (r != DWT2_OK) return r;
     g_last_error = DWT2_OK;
     return DWT2_OK;

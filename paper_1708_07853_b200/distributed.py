@@ -243,22 +243,44 @@ class StripPyramid:
 def strip_pyramid_step(pyr: StripPyramid, plan, overlap: bool = True, stream=None, exchange=None):
     """All levels of rank's strip: per level, the ghost-row exchange and the
     fused level kernel(s); with overlap, the interior quad rows run while the
-    ghost rows are in flight.  exchange(k) -> handle / finish(handle) may
-    replace the process-group exchange (single-GPU emulation in the tests)."""
+    ghost rows are in flight, then the two boundary quad rows.  exchange(k)
+    may replace the process-group exchange (single-GPU emulation in tests).
+
+    Measured on one B200 (scripts/strip_host_cost.py, config 3 at G = 8): the
+    boundary launch right behind the interior one (programmatic dependent
+    launch) costs no GPU time over a single launch of all rows (59 us per
+    step either way), and running it on a side stream instead adds ~30 us of
+    host enqueue time per level without saving GPU time -- so both parts stay
+    on the current stream."""
+    import torch
     from . import dwt2
+    # raw C-ABI arguments of every level, built once (a step then costs the
+    # launches' own host time, not Python tensor bookkeeping)
+    key = (id(plan), pyr.out.data_ptr())
+    if getattr(pyr, "_launch_key", None) != key:
+        args = []
+        for k in range(pyr.levels):
+            buf = pyr.bufs[k]
+            ll = pyr.owned(k + 1) if k + 1 < pyr.levels else None
+            args.append((buf.data_ptr(), buf.stride(0), 0 if ll is None else ll.data_ptr(),
+                         0 if ll is None else ll.stride(0)))
+        pyr._launch_args, pyr._launch_key = args, key
+    h = plan.handle
+    out = pyr.out.data_ptr()
+    sh = (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
+    launch = dwt2.dwt2_forward_strip_level
     for k in range(pyr.levels):
         reqs = pyr.start(k) if exchange is None else exchange(k)
-        ll = pyr.owned(k + 1) if k + 1 < pyr.levels else None
-        buf = pyr.bufs[k]
+        bp, bpitch, lp, lpitch = pyr._launch_args[k]
         if overlap:
-            plan.forward_level(k, buf, ll, pyr.out, dwt2.DWT2_STRIP_INTERIOR, stream)
+            launch(h, k, bp, bpitch, lp, lpitch, out, dwt2.DWT2_STRIP_INTERIOR, sh)
             if exchange is None:
                 pyr.finish(reqs)
-            plan.forward_level(k, buf, ll, pyr.out, dwt2.DWT2_STRIP_BOUNDARY, stream)
+            launch(h, k, bp, bpitch, lp, lpitch, out, dwt2.DWT2_STRIP_BOUNDARY, sh)
         else:
             if exchange is None:
                 pyr.finish(reqs)
-            plan.forward_level(k, buf, ll, pyr.out, dwt2.DWT2_STRIP_ALL, stream)
+            launch(h, k, bp, bpitch, lp, lpitch, out, dwt2.DWT2_STRIP_ALL, sh)
     return pyr.out
 
 

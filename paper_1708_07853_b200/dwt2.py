@@ -321,6 +321,10 @@ class StripPlan:
         self.ghost_bot = self.level_info[0].ghost_bot
 
     @property
+    def handle(self):
+        return self._p
+
+    @property
     def in_rows(self) -> int:
         return self.row_end - self.row_begin + self.ghost_top + self.ghost_bot
 

@@ -103,3 +103,33 @@ def test_strip_levels_rejects_misaligned():
         dwt2.StripPlan(64, 256, 0, 100, 3)        # row_end not a multiple of 8 and not H
     with pytest.raises(dwt2.DWT2Error):
         dwt2.StripPlan(64, 257, 256, 257, 8)      # a 1-row strip
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+def test_strip_pyramid_step_side_stream_config3_g8(overlap):
+    """The bench's per-rank step (strip_pyramid_step: interior on the current
+    stream, boundary on a side stream once the exchange is done) for every
+    rank of config 3 at G = 8, with the exchange emulated by copying the ghost
+    rows from the full image: bit-identical to the single-GPU transform."""
+    x = workloads.uniform_int(16384, 16384, 3)
+    H, W = x.shape
+    xt = torch.from_numpy(x).cuda()
+    full = np.full((H, W), np.nan, np.float32)
+    for g in range(8):
+        p = D.StripPyramid(W, H, g, 8, 1, device="cuda")
+        p.owned(0).copy_(xt[p.r0:p.r1])
+        plan = dwt2.StripPlan(W, H, p.r0, p.r1, 1)
+
+        def exchange(k, p=p):
+            lo, hi = p.global_rows(0)
+            if p.ghost_top:
+                p.bufs[0][0:2].copy_(xt[lo:lo + 2])
+            if p.ghost_bot:
+                p.bufs[0][-1].copy_(xt[hi - 1])
+            return []
+        D.strip_pyramid_step(p, plan, overlap=overlap, exchange=exchange)
+        torch.cuda.synchronize()
+        D.place_pyramid_output(full, p.out.cpu().numpy(), W, H, p.r0, p.r1, 1)
+        plan.close()
+    ref = dwt2.Plan(W, H, 1).forward(xt).cpu().numpy()
+    np.testing.assert_array_equal(full, ref)
