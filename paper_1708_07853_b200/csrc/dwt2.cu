@@ -153,7 +153,8 @@ struct alignas(64) LevelArgs {
     int out_q0;                       // global quad row stored at output row 0
     int nslabs, count;
     int qa0, qa1, qb0, qb1;           // quad-row ranges [qa0, qa1) and [qb0, qb1)
-    int tb;                           // quad rows per tile
+    int tb;                           // quad rows per tile (range A)
+    int tb_b;                         // quad rows per tile (range B)
     int nblk_a, nblk;                 // row blocks in range A, in A and B
     int ntiles;                       // count * nblk * nslabs
     int nwarps;                       // warps in the grid
@@ -295,8 +296,8 @@ __device__ __forceinline__ Tile decode_tile(const LevelArgs &a, int t)
         T.qa = a.qa0 + blk * a.tb;
         T.qb = imin(T.qa + a.tb, a.qa1);
     } else {
-        T.qa = a.qb0 + (blk - a.nblk_a) * a.tb;
-        T.qb = imin(T.qa + a.tb, a.qb1);
+        T.qa = a.qb0 + (blk - a.nblk_a) * a.tb_b;
+        T.qb = imin(T.qa + a.tb_b, a.qb1);
     }
     return T;
 }
@@ -861,6 +862,9 @@ struct TilePolicy {
     int tpw;       // target tiles per warp on large levels
     int min_tb;    // minimum quad rows per tile
     int min_tpw;   // below this many tiles per warp: one tile per warp, no queue
+    int guided;    // mid-size levels: large tiles first, small ones last (DWT2_GUIDED=0 disables)
+    int guided_a;  // percent of the rows in the large (one per warp) tiles
+    int guided_b;  // small tiles per warp for the rest
 };
 
 const TilePolicy &tile_policy()
@@ -875,6 +879,10 @@ const TilePolicy &tile_policy()
         pol.tpw = env("DWT2_TPW", DWT2_TPW);
         pol.min_tb = env("DWT2_MIN_TB", MIN_TILE_ROWS);
         pol.min_tpw = env("DWT2_MIN_TPW", DWT2_MIN_TPW);
+        const char *g = getenv("DWT2_GUIDED");
+        pol.guided = (g && g[0] == '0') ? 0 : 1;
+        pol.guided_a = env("DWT2_GUIDED_A", 70);
+        pol.guided_b = env("DWT2_GUIDED_B", 4);
     });
     return pol;
 }
@@ -956,8 +964,32 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     tb = std::max<long long>(PAIRS - 1, std::min<long long>(MAX_TILE_ROWS, tb));
     tb = std::max<long long>(PAIRS - 1, (tb + 1 + PAIRS - 1) / PAIRS * PAIRS - 1);
     a.tb = int(tb);
+    a.tb_b = int(tb);
     a.nblk_a = (lenA + a.tb - 1) / a.tb;
     a.nblk = a.nblk_a + (lenB + a.tb - 1) / a.tb;
+    // Guided tiles for mid-size levels (few tiles per warp): one large tile
+    // per warp over ~70 % of the rows first, then the rest as ~4 small tiles
+    // per warp from the queue, so warps on slower SMs (a 1.5x spread of SM
+    // throughput under full HBM load) do not set the kernel's length, while
+    // most rows still pay the carry-in row of a large tile only.
+    if (pol.guided && io.count == 1 && lenB == 0 && slab_rows >= 16LL * warps_full &&
+        slab_rows / ((long long)a.tb * warps_full) < 8) {
+        const long long nblk_a = std::max<long long>(1, warps_full / a.nslabs);
+        long long tb_a = (pol.guided_a * lenA / 100) / nblk_a;
+        tb_a = (tb_a + 1) / PAIRS * PAIRS - 1;                       // tb + 1 whole stages, rounded down
+        if (tb_a >= 2 * PAIRS - 1) {
+            const long long rows_a = nblk_a * tb_a, rest = lenA - rows_a;
+            long long tb_b = rest * a.nslabs / ((long long)pol.guided_b * warps_full);
+            tb_b = std::max<long long>(2 * PAIRS - 1, (tb_b + 1 + PAIRS - 1) / PAIRS * PAIRS - 1);
+            a.tb = int(tb_a);
+            a.tb_b = int(std::min<long long>(tb_b, MAX_TILE_ROWS));
+            a.qa1 = int(qa0 + rows_a);
+            a.qb0 = a.qa1;
+            a.qb1 = qa1;
+            a.nblk_a = int(nblk_a);
+            a.nblk = a.nblk_a + int((rest + a.tb_b - 1) / a.tb_b);
+        }
+    }
     const long long ntiles = (long long)io.count * a.nblk * a.nslabs;
     if (ntiles >= (1LL << 31)) return fail(DWT2_EINVAL);
     a.ntiles = int(ntiles);
