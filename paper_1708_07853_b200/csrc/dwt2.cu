@@ -104,8 +104,7 @@ constexpr int WARPS = DWT2_WARPS;           // warps per CTA (independent; packi
 constexpr int THREADS = WARPS * 32;
 constexpr int MIN_TILE_ROWS = 11;           // min quad rows per tile (sweep: 11 > 7, 15 on 4096^2 and 8192^2)
 constexpr int MAX_TILE_ROWS = 127;
-constexpr int MAX_COUNTERS = 2 * MAX_LEVELS;  // work-queue counter pairs: per level, and per level for strip
-                                              // BOUNDARY launches (which may run concurrently with INTERIOR)
+constexpr int MAX_COUNTERS = QUEUE_SLOTS;    // work-queue counter pairs (slots: dwt2_internal.h)
 
 // smem row pitch: TMA writes a box densely (136); the cp.async loader keeps
 // every row's 16-byte alignment shift delta (0..3 floats), hence 4 more.
@@ -997,7 +996,7 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     const int grid = int(std::max<long long>(1, std::min<long long>(max_ctas, want_ctas)));
     a.nwarps = grid * WARPS;
     a.static_tiles = ntiles <= a.nwarps ? 1 : 0;
-    a.counter = p->counters + 2 * (level + (queue ? MAX_LEVELS : 0));
+    a.counter = p->counters + 2 * ((queue ? QUEUE_STRIP_BOUNDARY : QUEUE_FORWARD) + level);
 
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));

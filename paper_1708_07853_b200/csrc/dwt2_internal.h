@@ -15,6 +15,13 @@ namespace dwt2_detail {
 
 constexpr int MAX_LEVELS = 32;
 
+// Work-queue counter pairs in dwt2_plan::counters (each level kernel's
+// self-resetting tile queue, see queue.cuh), by slot base + level:
+constexpr int QUEUE_FORWARD = 0;                  // forward level kernels (5/3 or K = 2)
+constexpr int QUEUE_STRIP_BOUNDARY = MAX_LEVELS;  // strip BOUNDARY launches (may overlap INTERIOR)
+constexpr int QUEUE_INVERSE = 2 * MAX_LEVELS;     // inverse level kernels
+constexpr int QUEUE_SLOTS = 3 * MAX_LEVELS;
+
 struct LevelGeom {
     int W, H;            // level input size
     int Wq, Hq;          // LL size: ceil(W / 2) x ceil(H / 2)

@@ -31,10 +31,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "dwt2_internal.h"
+#include "queue.cuh"
 
 using namespace dwt2_detail;
 
@@ -78,6 +80,8 @@ struct K2Args {
     long long ntiles;
     double c0, c1, c2, c3;                 // lifting coefficients (predict, update, predict, update)
     double sll, sd, shh;                   // output scaling: LL, HL / LH, HH
+    unsigned int *counter;                 // tile queue (queue.cuh)
+    int nwarps;
 };
 
 __device__ __forceinline__ int wssi(int k, int n)
@@ -361,10 +365,10 @@ __global__ void __launch_bounds__(KT, DWT2_K2_MINB) dwt_k2_level_kernel(const __
     extern __shared__ __align__(16) float k2_smem[];
     const int lane = threadIdx.x & 31;
     float *wring = k2_smem + (threadIdx.x >> 5) * (DS * 2 * RW);
-    const long long nwarps = (long long)gridDim.x * KW;
     const int Wq = (a.W + 1) >> 1, Hq = (a.H + 1) >> 1;
     const long long per_img = (long long)a.nblk * a.nslabs;
-    for (long long t = (long long)blockIdx.x * KW + (threadIdx.x >> 5); t < a.ntiles; t += nwarps) {
+    for (long long t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane); t < a.ntiles;
+         t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane)) {
         const int img = int(t / per_img);
         const int rr = int(t - img * per_img);
         const int blk = rr / a.nslabs;
@@ -417,13 +421,18 @@ int32_t launch_k2_level(const dwt2_plan *p, K2Args a, cudaStream_t s)
     a.nslabs = (Wq + OUTQ - 1) / OUTQ;
     const long long warps = (long long)p->sms * k2_ctas_per_sm() * KW;
     const long long slab_rows = (long long)a.count * a.nslabs * Hq;
-    long long tb = slab_rows / (4 * warps);                   // ~4 tiles per resident warp
+    // ~16 tiles per resident warp through the queue (measured: 0.62 -> 0.77
+    // of copy at 16384^2 against 4; the 4 warm-up rows per tile cost less
+    // than the imbalance), scripts/sweeps/gpu_queue_tpw.sh
+    static const int tpw = [] { const char *v = getenv("DWT2_K2_TPW"); return v && atoi(v) > 0 ? atoi(v) : 16; }();
+    long long tb = slab_rows / (tpw * warps);
     tb = std::max<long long>(16, std::min<long long>(512, tb)); // 4 warm-up rows per tile: >= 16 rows
     a.tb = int(tb);
     a.nblk = int((Hq + tb - 1) / tb);
     a.ntiles = (long long)a.count * a.nblk * a.nslabs;
     const long long want = (a.ntiles + KW - 1) / KW;
     const int grid = int(std::max<long long>(1, std::min<long long>(want, warps / KW)));
+    a.nwarps = grid * KW;
     const bool vec = aligned(a.in, 16) && a.in_pitch % 4 == 0 && (a.count == 1 || a.in_img % 4 == 0) &&
                      aligned(a.ll, 4 * QK) && aligned(a.hl, 4 * QK) && aligned(a.lh, 4 * QK) && aligned(a.hh, 4 * QK) &&
                      a.ll_pitch % QK == 0 && a.out_pitch % QK == 0 &&
@@ -479,6 +488,8 @@ struct K2InvArgs {
     double c0, c1, c2, c3, K2sq, invK2sq;  // K^2 and 1 / K^2
     int async;                             // 1: every plane 8-byte aligned with even pitches (cp.async ring)
     int vec_out;                           // 1: output 16-byte aligned with pitch % 4 == 0 (float4 stores)
+    unsigned int *counter;                 // tile queue (queue.cuh)
+    int nwarps;
 };
 
 struct InvCarry {
@@ -694,10 +705,10 @@ __global__ void __launch_bounds__(KT, 4) dwt_k2_inverse_kernel(const __grid_cons
     pdl_wait97();
     const int lane = threadIdx.x & 31;
     float *ring = kinv_smem + (threadIdx.x >> 5) * (IDSK * 4 * 64);
-    const long long nwarps = (long long)gridDim.x * KW;
     const int Wq = (a.W + 1) >> 1, Hq = (a.H + 1) >> 1;
     const long long per_img = (long long)a.nblk * a.nslabs;
-    for (long long t = (long long)blockIdx.x * KW + (threadIdx.x >> 5); t < a.ntiles; t += nwarps) {
+    for (long long t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane); t < a.ntiles;
+         t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane)) {
         const int img = int(t / per_img);
         const int rr = int(t - img * per_img);
         const int blk = rr / a.nslabs;
@@ -730,13 +741,15 @@ int32_t launch_k2_inverse_level(const dwt2_plan *p, K2InvArgs a, cudaStream_t s)
     a.nslabs = (Wq + OUTQ - 1) / OUTQ;
     const long long warps = (long long)p->sms * per_sm * KW;
     const long long slab_rows = (long long)a.count * a.nslabs * Hq;
-    long long tb = slab_rows / (4 * warps);
+    static const int tpw = [] { const char *v = getenv("DWT2_K2INV_TPW"); return v && atoi(v) > 0 ? atoi(v) : 8; }();
+    long long tb = slab_rows / (tpw * warps);
     tb = std::max<long long>(16, std::min<long long>(512, tb));
     a.tb = int(tb);
     a.nblk = int((Hq + tb - 1) / tb);
     a.ntiles = (long long)a.count * a.nblk * a.nslabs;
     const long long want = (a.ntiles + KW - 1) / KW;
     const int grid = int(std::max<long long>(1, std::min<long long>(want, warps / KW)));
+    a.nwarps = grid * KW;
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(grid);
@@ -804,6 +817,7 @@ int32_t run_levels_k2(const dwt2_plan *p, const float *in, float *out, int count
             a.ll_pitch = p->sc_pitch[si];
             a.ll_img = p->sc_img_stride[si];
         }
+        a.counter = p->counters + 2 * (QUEUE_FORWARD + k);
         int32_t r = launch_k2_level(p, a, s);
         if (r != DWT2_OK) return r;
     }
@@ -851,6 +865,7 @@ int32_t run_inverse_k2(const dwt2_plan *p, const float *in, float *out, int coun
             a.out_pitch = p->sc_pitch[si];
             a.out_img = p->sc_img_stride[si];
         }
+        a.counter = p->counters + 2 * (QUEUE_INVERSE + k);
         int32_t r = launch_k2_inverse_level(p, a, s);
         if (r != DWT2_OK) return r;
     }

@@ -35,10 +35,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "dwt2_internal.h"
+#include "queue.cuh"
 
 using namespace dwt2_detail;
 
@@ -58,6 +60,8 @@ struct InvArgs {
     int nslabs, nblk, tb, count;
     long long ntiles;
     const float *ll_lo, *ll_hi, *d_lo, *d_hi;   // allocation ranges of the LL / detail sources (ring loader)
+    unsigned int *counter;                       // tile queue (queue.cuh)
+    int nwarps;
 };
 
 // Raw coefficients of one quad row as one lane sees them: its 2 quads and,
@@ -212,9 +216,9 @@ __global__ void __launch_bounds__(ITHREADS, 2) dwt53_inverse_level_kernel(const 
     pdl_launch_inv();
     pdl_wait_inv();
     const int lane = threadIdx.x & 31;
-    const long long nwarps = (long long)gridDim.x * IWARPS;
     const int Wq = (a.W + 1) >> 1, Hq = (a.H + 1) >> 1;
-    for (long long t = (long long)blockIdx.x * IWARPS + (threadIdx.x >> 5); t < a.ntiles; t += nwarps) {
+    for (long long t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane); t < a.ntiles;
+         t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane)) {
         // tiles: image-major, then row block, then slab (adjacent slabs run together)
         const long long per_img = (long long)a.nblk * a.nslabs;
         const int img = int(t / per_img);
@@ -424,10 +428,10 @@ __global__ void __launch_bounds__(IRW * 32, 3) dwt53_inverse_ring_kernel(const _
     pdl_wait_inv();
     const int lane = threadIdx.x & 31;
     float *ring = iring_smem + (threadIdx.x >> 5) * (IDS * ISTAGE);
-    const long long nwarps = (long long)gridDim.x * IRW;
-    const int Wq = (a.W + 1) >> 1, Hq = (a.H + 1) >> 1;
+    const int Hq = (a.H + 1) >> 1;
     const long long per_img = (long long)a.nblk * a.nslabs;
-    for (long long t = (long long)blockIdx.x * IRW + (threadIdx.x >> 5); t < a.ntiles; t += nwarps) {
+    for (long long t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane); t < a.ntiles;
+         t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane)) {
         const int img = int(t / per_img);
         const int r = int(t - (long long)img * per_img);
         const int blk = r / a.nslabs;
@@ -487,13 +491,19 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
     if (ring) {
         const long long rwarps = (long long)p->sms * inverse_ring_ctas_per_sm() * IRW;
         const long long slab_rows = (long long)a.count * a.nslabs * Hq;
-        long long tb = slab_rows / (8 * rwarps);
+        // tiles per warp for the queue: 16 on large levels (balance), 4 on
+        // mid-size ones (the seed row of a tile costs more there); measured,
+        // scripts/sweeps/gpu_queue_tpw.sh
+        static const int env_tpw = [] { const char *v = getenv("DWT2_INV_TPW"); return v ? atoi(v) : 0; }();
+        const int tpw = env_tpw > 0 ? env_tpw : (slab_rows >= 256 * rwarps ? 16 : 4);
+        long long tb = slab_rows / (tpw * rwarps);
         tb = std::max<long long>(8, std::min<long long>(256, tb));
         a.tb = int(tb);
         a.nblk = int((Hq + tb - 1) / tb);
         a.ntiles = (long long)a.count * a.nblk * a.nslabs;
         const long long want = (a.ntiles + IRW - 1) / IRW;
         const int grid = int(std::max<long long>(1, std::min<long long>(want, rwarps / IRW)));
+        a.nwarps = grid * IRW;
         cudaLaunchConfig_t cfg;
         memset(&cfg, 0, sizeof(cfg));
         cfg.gridDim = dim3(grid);
@@ -522,6 +532,7 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
     a.ntiles = (long long)a.count * a.nblk * a.nslabs;
     const long long want = (a.ntiles + IWARPS - 1) / IWARPS;
     const int grid = int(std::max<long long>(1, std::min<long long>(want, warps / IWARPS)));
+    a.nwarps = grid * IWARPS;
     const bool vec = aligned(a.ll, 8) && aligned(a.hl, 8) && aligned(a.lh, 8) && aligned(a.hh, 8) &&
                      a.ll_pitch % 2 == 0 && a.d_pitch % 2 == 0 && (a.count == 1 || (a.ll_img % 2 == 0 && a.d_img % 2 == 0)) &&
                      aligned(a.out, 16) && a.out_pitch % 4 == 0 && (a.count == 1 || a.out_img % 4 == 0);
@@ -592,6 +603,7 @@ int32_t run_inverse(const dwt2_plan *p, const float *in, float *out, int count, 
             a.ll_lo = p->scratch[sidx];
             a.ll_hi = p->scratch[sidx] + (long long)count * p->sc_img_stride[sidx];
         }
+        a.counter = p->counters + 2 * (QUEUE_INVERSE + k);
         int32_t r = launch_inverse_level(p, a, s);
         if (r != DWT2_OK) return r;
     }
