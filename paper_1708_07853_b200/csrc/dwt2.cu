@@ -864,7 +864,6 @@ struct TilePolicy {
     int guided;    // mid-size levels: large tiles first, small ones last (DWT2_GUIDED=0 disables)
     int guided_a;  // percent of the rows in the large (one per warp) tiles
     int guided_b;  // small tiles per warp for the rest
-    int tail;      // experiment: percent of a large level's rows in small tiles at the end of the queue
 };
 
 const TilePolicy &tile_policy()
@@ -883,8 +882,6 @@ const TilePolicy &tile_policy()
         pol.guided = (g && g[0] == '0') ? 0 : 1;
         pol.guided_a = env("DWT2_GUIDED_A", 70);
         pol.guided_b = env("DWT2_GUIDED_B", 4);
-        const char *t = getenv("DWT2_TAIL");
-        pol.tail = t ? atoi(t) : 0;
     });
     return pol;
 }
@@ -990,21 +987,6 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
             a.qb1 = qa1;
             a.nblk_a = int(nblk_a);
             a.nblk = a.nblk_a + int((rest + a.tb_b - 1) / a.tb_b);
-        }
-    }
-    // Optional small tiles at the end of the queue on large levels (experiment,
-    // DWT2_TAIL=<percent of rows>; off by default)
-    if (pol.tail > 0 && a.tb == a.tb_b && io.count == 1 && lenB == 0 && a.tb > 2 * PAIRS - 1) {
-        long long rows_b = lenA * pol.tail / 100;
-        long long rows_a = (lenA - rows_b) / a.tb * a.tb;
-        rows_b = lenA - rows_a;
-        if (rows_a > 0 && rows_b > 0) {
-            a.tb_b = 2 * PAIRS - 1;
-            a.qa1 = int(qa0 + rows_a);
-            a.qb0 = a.qa1;
-            a.qb1 = qa1;
-            a.nblk_a = int(rows_a / a.tb);
-            a.nblk = a.nblk_a + int((rows_b + a.tb_b - 1) / a.tb_b);
         }
     }
     const long long ntiles = (long long)io.count * a.nblk * a.nslabs;
