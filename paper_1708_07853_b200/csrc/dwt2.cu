@@ -15,13 +15,16 @@
 // written per pixel.  See DESIGN.md sections 5-6 for the layout and roofline.
 //
 // Work decomposition.  A warp owns a 128-pixel column slab (64 quads, 2 per
-// lane) and walks DOWN it, row pair by row pair, carrying the predicted
-// values of the previous quad row in registers.  A CTA is WARPS adjacent
-// slabs (a 512-pixel "group") over the same quad rows, so the 8 halo columns
-// its warps share are re-read from L2 at the same time.  The grid is
-// persistent: the (image x group x quad-row) space is cut into one
-// contiguous, balanced range per CTA, so every CTA finishes together and
-// vertical halos (2 rows above, 1 below) are paid once per range.
+// lane) and walks DOWN a tile of tb quad rows, row pair by row pair,
+// carrying the predicted values of the previous quad row in registers.  The
+// grid is persistent (4 warps per CTA, 4 CTAs per SM); warps are independent
+// and take tiles from a self-resetting atomic queue in row-block-major order
+// (horizontally adjacent tiles run together and share their halo columns in
+// L2), prefetching the next tile's stages while finishing the current one.
+// The queue exists because SMs differ by up to 1.5x in throughput under full
+// HBM load; mid-size levels use guided tiles (one large tile per warp, then
+// small ones) and small levels one static tile per warp (see tile_policy and
+// launch_level).
 //
 // Arithmetic: fp32 in HBM, fp64 in registers.  Every CDF 5/3 coefficient is
 // dyadic, so fp64 evaluation of fp32 inputs is exact in practice and the
