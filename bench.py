@@ -581,8 +581,12 @@ def main():
     # dominant kernel (level 1) duration
     k_ms = runner.level1_kernel_ms(max(3, args.steps))
     if k_ms is None:
-        # one-level configs: the level (all its step kernels for a scheme) is the step
-        k_ms = ms / max(1, (runner.launches // SCHEME_STEPS[args.scheme] if runner.mode != "strip" else 1))
+        # one-level configs: the level (all its step kernels for a scheme) is the step;
+        # row strips: level 1's share of the step by algorithmic bytes (the exchange included)
+        if runner.mode == "strip":
+            k_ms = ms * runner.level1_bytes / max(1, runner.algo_bytes)
+        else:
+            k_ms = ms / max(1, runner.launches // SCHEME_STEPS[args.scheme])
     k_bytes = runner.level1_bytes
     achieved = k_bytes / (k_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
