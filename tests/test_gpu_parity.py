@@ -255,3 +255,44 @@ def test_negative_control_checker_flags_one_ulp():
         with pytest.raises(AssertionError):
             compare(bad, None, ref_ii, True, "perturbed")
     assert ulp32(np.array([1.0]))[0] > 0
+
+
+def test_errors_extended_api():
+    """Argument checks of the entry points added for the 8f rows: strip
+    levels, batched inverse, schemes, lifting plans; a failing call sets
+    dwt2_last_error and a good call clears it."""
+    s = torch.cuda.current_stream().cuda_stream
+    lib = dwt2.lib()
+    # strip level: bad level index, missing ll_out for a non-last level, part out of range
+    sp = dwt2.StripPlan(64, 256, 0, 128, 2)
+    buf = torch.zeros(129, 64, device="cuda")
+    out = torch.zeros(128, 64, device="cuda")
+    ll = torch.zeros(70, 32, device="cuda")
+    for args in [(5, buf.data_ptr(), 64, ll.data_ptr(), 32, out.data_ptr(), 0),     # level 5 of a 2-level plan
+                 (0, buf.data_ptr(), 64, 0, 0, out.data_ptr(), 0),                  # level 0 needs ll_out
+                 (0, buf.data_ptr(), 64, ll.data_ptr(), 32, out.data_ptr(), 3),     # part 3
+                 (0, buf.data_ptr(), 32, ll.data_ptr(), 32, out.data_ptr(), 0)]:    # in_pitch < width
+        with pytest.raises(dwt2.DWT2Error):
+            dwt2.dwt2_forward_strip_level(sp.handle, *args[:6], args[6], s)
+        assert lib.dwt2_last_error() == dwt2.DWT2_EINVAL
+    with pytest.raises(dwt2.DWT2Error):          # the one-level entry point on a 2-level strip plan
+        dwt2.dwt2_forward_strip(sp.handle, buf.data_ptr(), out.data_ptr(), 0, s)
+    sp.close()
+    # batched inverse / scheme: count above the plan's max_count, unknown scheme
+    plan = dwt2.Plan(64, 64, 1, max_count=2)
+    a = torch.zeros(3, 64, 64, device="cuda")
+    b = torch.zeros(3, 64, 64, device="cuda")
+    with pytest.raises(dwt2.DWT2Error):
+        dwt2.dwt2_inverse_batched(plan.handle, a.data_ptr(), b.data_ptr(), 3, 4096, 4096, s)
+    with pytest.raises(dwt2.DWT2Error):
+        dwt2.dwt2_forward_scheme(plan.handle, 42, a.data_ptr(), b.data_ptr(), 1, 4096, 4096, s)
+    dwt2.dwt2_forward_scheme(plan.handle, dwt2.SCHEMES["sep_lifting"], a.data_ptr(), b.data_ptr(), 2, 4096, 4096, s)
+    assert lib.dwt2_last_error() == dwt2.DWT2_OK
+    plan.close()
+    # wavelet plans: out-of-range wavelet id; strip plans are 5/3 only by construction
+    with pytest.raises(dwt2.DWT2Error):
+        dwt2.dwt2_plan_create_ex(64, 64, 1, 0, 9, 1)
+    with pytest.raises(dwt2.DWT2Error) as e:
+        dwt2.Plan(64, 64, 1, wavelet="cdf97").forward_host(torch.zeros(64, 64).pin_memory(),
+                                                           torch.zeros(64, 64).pin_memory())
+    assert e.value.code == dwt2.DWT2_EUNSUPPORTED
