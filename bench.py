@@ -39,10 +39,10 @@ UNIT = "Gpixel/s"
 BYTES_PER_PX = 8            # algorithmic: 4 B read + 4 B written per pixel per level
 # algorithmic bytes per pixel per level of the comparison schemes (each step one HBM pass; the in-place
 # separable steps 2-4 read 4 B and write 2 B): see scripts/scheme_compare.py, DESIGN.md 5.3
-SCHEME_BYTES = {"fused": 8, "nonsep_naive": 8, "nonsep_lifting": 16, "nonsep_adapted": 16, "sep_conv": 16,
-                "sep_lifting": 26}
-SCHEME_STEPS = {"fused": 1, "nonsep_naive": 1, "nonsep_lifting": 2, "nonsep_adapted": 2, "sep_conv": 2,
-                "sep_lifting": 4}
+SCHEME_BYTES = {"fused": 8, "fused_literal": 8, "fused_adapted": 8, "nonsep_naive": 8, "nonsep_lifting": 16,
+                "nonsep_adapted": 16, "sep_conv": 16, "sep_lifting": 26}
+SCHEME_STEPS = {"fused": 1, "fused_literal": 1, "fused_adapted": 1, "nonsep_naive": 1, "nonsep_lifting": 2,
+                "nonsep_adapted": 2, "sep_conv": 2, "sep_lifting": 4}
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
 
 
@@ -83,8 +83,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--op", default="forward", choices=["forward", "inverse"],
                     help="inverse: time the inverse transform (SURVEY 8f N2) of the config's pyramid")
-    ap.add_argument("--scheme", default="fused", choices=["fused", "nonsep_naive", "nonsep_lifting", "nonsep_adapted",
-                                                        "sep_conv", "sep_lifting"],
+    ap.add_argument("--scheme", default="fused", choices=["fused", "fused_literal", "fused_adapted", "nonsep_naive",
+                                                        "nonsep_lifting", "nonsep_adapted", "sep_conv", "sep_lifting"],
                     help="forward with one of the paper's schemes, one kernel per step (SURVEY 8f N1)")
     ap.add_argument("--wavelet", default="cdf53", choices=["cdf53", "cdf97"],
                     help="cdf97: the K = 2 non-separable kernel (SURVEY 8f N4); single-image and batch configs")

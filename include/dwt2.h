@@ -222,14 +222,18 @@ int32_t dwt2_inverse_batched(const dwt2_plan *plan, const float *in, float *out,
 /* Schemes of the paper, for the comparison of SURVEY.md 8f row N1 (PAPER.md
  * section 4, Fig. 6): the same transform computed with one kernel per
  * barrier-separated step of each scheme (a step boundary that exchanges
- * data across the image is a kernel boundary, i.e. an HBM round trip). */
+ * data across the image is a kernel boundary, i.e. an HBM round trip), and
+ * the fused single-step kernel with the literal and the adapted arithmetic
+ * (the paper's operation-count trade-off at a fixed number of steps). */
 enum {
     DWT2_SCHEME_FUSED = 0,          /* Eq. (5) fused into one kernel per level (the product path) */
     DWT2_SCHEME_NONSEP_NAIVE = 1,   /* Eq. (5), one plain kernel, predicted neighbours recomputed */
     DWT2_SCHEME_NONSEP_LIFTING = 2, /* Eq. (5): spatial predict | spatial update (2 kernels) */
     DWT2_SCHEME_NONSEP_ADAPTED = 3, /* Fig. 3: Eq. (5) with the constants P0, U0 split off (2 kernels) */
     DWT2_SCHEME_SEP_CONV = 4,       /* Eq. (4): horizontal | vertical filter bank (2 kernels) */
-    DWT2_SCHEME_SEP_LIFTING = 5     /* Eq. (3): 4 separable lifting steps (4 kernels) */
+    DWT2_SCHEME_SEP_LIFTING = 5,    /* Eq. (3): 4 separable lifting steps (4 kernels) */
+    DWT2_SCHEME_FUSED_LITERAL = 6,  /* the fused kernel with Eq. (5)'s operators as printed (24 MACs / quad) */
+    DWT2_SCHEME_FUSED_ADAPTED = 7   /* the fused kernel with Fig. 3's adapted arithmetic (18 MACs / quad) */
 };
 
 /* Kernel launches (barrier-separated steps) per level of a scheme, or

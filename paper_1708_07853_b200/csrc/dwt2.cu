@@ -424,8 +424,17 @@ __device__ __forceinline__ RowD load_row(const float *p, int lane, const EdgeFla
 // registers from the previous quad row (Carry).
 struct Carry {
     real lh[QPL], hh[QPL];            // LH and HH' of quad row n-1
+    real lhp[QPL];                    // LH' of quad row n-1 (literal / adapted arithmetic only)
     real hh_halo;                     // HH' of the halo quad m0-1 at n-1 (lane 0)
 };
+
+// Arithmetic of the spatial steps (the same operators, evaluated three ways;
+// all exact in the fp64 registers for these data, so bit-identical results):
+//   AR_GROUPED  separable grouping, 16 DP ops per quad (the product path)
+//   AR_LITERAL  Eq. (5) as printed: PP* and UU* as 4-term stencils, 24 MACs
+//   AR_ADAPTED  Fig. 3: P = P0 + P1, U = U0 + U1, non-separable N(P1), N(U1)
+//               then the quad-local constants C_H, C_V (18 MACs)
+enum { AR_GROUPED = 0, AR_LITERAL = 1, AR_ADAPTED = 2 };
 
 struct Out {
     float A[QPL], B[QPL], C[QPL], D[QPL];
@@ -434,10 +443,133 @@ struct Out {
 // Returns the outputs of quad row n; updates the carry to row n.
 // missing_odd: odd H, n is the last quad row (row 2n+1 does not exist):
 // LH', HH' := their values at n-1 (H[M] := H[M-1]).
-template <bool EDGE>
+template <bool EDGE, int AR>
+__device__ __forceinline__ Out predict_update_literal(const RowD &E, const RowD &O, const RowD &N, Carry &cy,
+                                                      int lane, const EdgeFlags &ef, bool carry_in, bool missing_odd)
+{
+    // Eq. (5) literally (AR_LITERAL) or in the adapted form of Fig. 3
+    // (AR_ADAPTED).  Same boundary rules as the grouped path: raw samples
+    // mirrored in load_row (even right / bottom edges), predicted values
+    // mirrored here (H[-1] := H[0] left / top, H[M] := H[M-1] odd edges).
+    real cp[QPL], dp[QPL], bp[QPL];
+#pragma unroll
+    for (int i = 0; i < QPL; ++i) {
+        const real a = E.v[2 * i], b = E.v[2 * i + 1], c = O.v[2 * i], d = O.v[2 * i + 1];
+        const real ar = (i < QPL - 1) ? E.v[2 * i + 2] : E.r;
+        const real cr = (i < QPL - 1) ? O.v[2 * i + 2] : O.r;
+        const real ad = N.v[2 * i], bd = N.v[2 * i + 1];
+        const real ard = (i < QPL - 1) ? N.v[2 * i + 2] : N.r;
+        if (AR == AR_LITERAL) {
+            bp[i] = fma(R_(-0.5), a + ar, b);                                     // HL' = b + P a
+            cp[i] = fma(R_(-0.5), a + ad, c);                                     // LH' = c + P* a
+            dp[i] = fma(R_(0.25), (a + ar) + (ad + ard),                          // HH' = d + P c + P* b + PP* a
+                        fma(R_(-0.5), b + bd, fma(R_(-0.5), c + cr, d)));
+        } else {
+            const real b1 = fma(R_(-0.5), ar, b);                                 // N(P1): HL += P1 LL
+            const real c1 = fma(R_(-0.5), ad, c);                                 //        LH += P1* LL
+            const real d1 = fma(R_(0.25), ard, fma(R_(-0.5), bd, fma(R_(-0.5), cr, d)));
+            const real b2 = fma(R_(-0.5), a, b1);                                 // C_H(P0)
+            const real d2 = fma(R_(-0.5), c1, d1);
+            cp[i] = fma(R_(-0.5), a, c1);                                         // C_V(P0*)
+            dp[i] = fma(R_(-0.5), b2, d2);
+            bp[i] = b2;
+        }
+    }
+    // halo quad m0 - 1 (columns x0-2, x0-1), literal form for both variants
+    real hbp = fma(R_(-0.5), E.l0 + E.v[0], E.l1);
+    real hdp = fma(R_(0.25), (E.l0 + E.v[0]) + (N.l0 + N.v[0]),
+                   fma(R_(-0.5), E.l1 + N.l1, fma(R_(-0.5), O.l0 + O.v[0], O.l1)));
+    if (missing_odd) {
+#pragma unroll
+        for (int i = 0; i < QPL; ++i) {
+            dp[i] = cy.hh[i];
+            cp[i] = cy.lhp[i];
+        }
+        hdp = cy.hh_halo;
+    }
+    // n-1 neighbours (carry) and their m-1 neighbours, captured before the carry moves on
+    real hu[QPL], lpu[QPL];
+#pragma unroll
+    for (int i = 0; i < QPL; ++i) {
+        hu[i] = cy.hh[i];
+        lpu[i] = cy.lhp[i];
+    }
+    real hu_halo = cy.hh_halo;
+    if (carry_in) {            // the first pair of a tile: row n-1 is this row (or the top mirror)
+#pragma unroll
+        for (int i = 0; i < QPL; ++i) {
+            hu[i] = dp[i];
+            lpu[i] = cp[i];
+        }
+        hu_halo = hdp;
+    }
+    const real bl_sh = __shfl_up_sync(0xffffffffu, bp[QPL - 1], 1);
+    const real dl_sh = __shfl_up_sync(0xffffffffu, dp[QPL - 1], 1);
+    const real dul_sh = __shfl_up_sync(0xffffffffu, hu[QPL - 1], 1);
+    real bl = (lane == 0) ? hbp : bl_sh;
+    real dl = (lane == 0) ? hdp : dl_sh;
+    real dul = (lane == 0) ? hu_halo : dul_sh;
+    if (EDGE) {
+        if (ef.left_edge) {            // H[-1] := H[0]
+            bl = bp[0];
+            dl = dp[0];
+            dul = hu[0];
+        }
+        if (!ef.evenW) {
+#pragma unroll
+            for (int i = 0; i < QPL; ++i) {
+                if (ef.last == i) {
+                    bp[i] = (i == 0) ? bl : bp[i - 1];
+                    dp[i] = (i == 0) ? dl : dp[i - 1];
+                }
+            }
+            if (carry_in) {    // the mirrored last column's HH' is row n-1's too
+#pragma unroll
+                for (int i = 0; i < QPL; ++i) hu[i] = dp[i];
+            }
+        }
+    }
+    Out o;
+#pragma unroll
+    for (int i = 0; i < QPL; ++i) {
+        const real a = E.v[2 * i];
+        const real hll = (i == 0) ? bl : bp[i - 1];          // HL'[m-1]
+        const real hhl = (i == 0) ? dl : dp[i - 1];          // HH'[m-1]
+        const real hhul = (i == 0) ? dul : hu[i - 1];        // HH'[m-1, n-1]
+        real A, B, C;
+        if (AR == AR_LITERAL) {
+            // LL = a + U HL' + U* LH' + UU* HH',  HL = HL' + U* HH',  LH = LH' + U HH'
+            A = fma(R_(0.0625), (dp[i] + hhl) + (hu[i] + hhul),
+                    fma(R_(0.25), cp[i] + lpu[i], fma(R_(0.25), bp[i] + hll, a)));
+            B = fma(R_(0.25), dp[i] + hu[i], bp[i]);
+            C = fma(R_(0.25), dp[i] + hhl, cp[i]);
+        } else {
+            // N(U1): LL += U1 HL + U1* LH + U1 U1* HH, HL += U1* HH, LH += U1 HH
+            const real ll1 = fma(R_(0.0625), hhul, fma(R_(0.25), lpu[i], fma(R_(0.25), hll, a)));
+            const real hl1 = fma(R_(0.25), hu[i], bp[i]);
+            const real lh1 = fma(R_(0.25), hhl, cp[i]);
+            const real ll2 = fma(R_(0.25), hl1, ll1);        // C_H(U0): LL += U0 HL, LH += U0 HH
+            C = fma(R_(0.25), dp[i], lh1);
+            A = fma(R_(0.25), C, ll2);                       // C_V(U0*): LL += U0* LH, HL += U0* HH
+            B = fma(R_(0.25), dp[i], hl1);
+        }
+        o.A[i] = to_f32(A);
+        o.B[i] = to_f32(B);
+        o.C[i] = to_f32(C);
+        o.D[i] = to_f32(dp[i]);
+        cy.lh[i] = C;
+        cy.hh[i] = dp[i];
+        cy.lhp[i] = cp[i];
+    }
+    cy.hh_halo = hdp;
+    return o;
+}
+
+template <bool EDGE, int AR = AR_GROUPED>
 __device__ __forceinline__ Out predict_update(const RowD &E, const RowD &O, const RowD &N, Carry &cy, int lane,
                                               const EdgeFlags &ef, bool carry_in, bool missing_odd)
 {
+    if (AR != AR_GROUPED) return predict_update_literal<EDGE, AR>(E, O, N, cy, lane, ef, carry_in, missing_odd);
     real cp[QPL], dp[QPL], bp[QPL];
 #pragma unroll
     for (int i = 0; i < QPL; ++i) {
@@ -534,7 +666,7 @@ __device__ __forceinline__ void storeq(float *p, const float (&x)[QPL], int n, b
 // streams tiles from the work queue through its own TMA ring (producer and
 // consumer in one warp, prefetching across tile boundaries).
 // ---------------------------------------------------------------------------
-template <bool TMA, bool VEC>
+template <bool TMA, bool VEC, int AR>
 __global__ void __launch_bounds__(THREADS, DWT2_MINB)
 dwt53_level_kernel(const __grid_constant__ LevelArgs a)
 {
@@ -757,7 +889,7 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
                     for (int i = 0; i < PAIRS; ++i) {
                         const RowD O = load_row<TMA, EG>(rowp(2 * i + 1), lane, ef, false);
                         const RowD N = load_row<TMA, EG>(rowp(2 * i + 2), lane, ef, true);
-                        const Out o = predict_update<EG>(E, O, N, cy, lane, ef, false, false);
+                        const Out o = predict_update<EG, AR>(E, O, N, cy, lane, ef, false, false);
                         storeq<VEC, EG>(pll, o.A, nL, false);
                         storeq<VEC, EG>(phl, o.B, nH, true);
                         storeq<VEC, EG>(plh, o.C, nL, true);
@@ -783,7 +915,7 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
                         }
                         // carry-in pair: quad row qa-1 (or row -1 mirroring row 0 at the top)
                         const bool cin = (kk == 0);
-                        const Out o = predict_update<EG>(E, O, N, cy, lane, ef, cin, !has_odd);
+                        const Out o = predict_update<EG, AR>(E, O, N, cy, lane, ef, cin, !has_odd);
                         if (!(cin && !top)) {
                             storeq<VEC, true>(pll, o.A, nL, false);
                             storeq<VEC, true>(phl, o.B, nH, true);
@@ -833,10 +965,18 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode()
 
 typedef void (*KernelFn)(LevelArgs);
 
-KernelFn kernel_for(bool tma, bool vec)
+template <int AR>
+KernelFn kernel_for_ar(bool tma, bool vec)
 {
-    if (tma) return vec ? dwt53_level_kernel<true, true> : dwt53_level_kernel<true, false>;
-    return vec ? dwt53_level_kernel<false, true> : dwt53_level_kernel<false, false>;
+    if (tma) return vec ? dwt53_level_kernel<true, true, AR> : dwt53_level_kernel<true, false, AR>;
+    return vec ? dwt53_level_kernel<false, true, AR> : dwt53_level_kernel<false, false, AR>;
+}
+
+KernelFn kernel_for(bool tma, bool vec, int ar = AR_GROUPED)
+{
+    if (ar == AR_LITERAL) return kernel_for_ar<AR_LITERAL>(tma, vec);
+    if (ar == AR_ADAPTED) return kernel_for_ar<AR_ADAPTED>(tma, vec);
+    return kernel_for_ar<AR_GROUPED>(tma, vec);
 }
 
 }  // namespace
@@ -890,7 +1030,7 @@ const TilePolicy &tile_policy()
 }
 
 int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO &io, int qa0, int qa1, int qb0,
-                     int qb1, cudaStream_t stream, int queue = 0)
+                     int qb1, cudaStream_t stream, int queue = 0, int ar = AR_GROUPED)
 {
     LevelArgs a;
     memset(&a, 0, sizeof(a));
@@ -1012,7 +1152,7 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel_for(tma, vec), a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel_for(tma, vec, ar), a);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(DWT2_ECUDA);
@@ -1028,6 +1168,15 @@ int32_t configure_kernels(int *max_ctas)
     std::call_once(once, [] {
         KernelFn fns[4] = {kernel_for(true, true), kernel_for(true, false), kernel_for(false, true),
                            kernel_for(false, false)};
+        for (int ar = AR_LITERAL; ar <= AR_ADAPTED; ++ar)
+            for (int t = 0; t < 4; ++t) {
+                const size_t smem = t < 2 ? Ring<true>::SMEM : Ring<false>::SMEM;
+                if (cudaFuncSetAttribute(kernel_for(t < 2, (t & 1) == 0, ar), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem)) != cudaSuccess) {
+                    status = DWT2_ECUDA;
+                    return;
+                }
+            }
         int dev = 0, sms = 0, per_sm = 0;
         if (cudaGetDevice(&dev) != cudaSuccess ||
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
@@ -1182,7 +1331,7 @@ namespace {
 // Forward of levels [first, last] for `count` images.  Level 1 reads `in`.
 // Level-1 quad rows may be restricted to [q1a, q1b) (host pipelining).
 int32_t run_levels(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,
-                   long long out_stride, int first, int last, int q1a, int q1b, cudaStream_t s)
+                   long long out_stride, int first, int last, int q1a, int q1b, cudaStream_t s, int ar = AR_GROUPED)
 {
     for (int k = first; k <= last; ++k) {
         const LevelGeom &g = p->geom[k];
@@ -1224,7 +1373,7 @@ int32_t run_levels(const dwt2_plan *p, const float *in, float *out, int count, l
             qa = q1a;
             qb = q1b;
         }
-        int32_t r = launch_level(p, k, g.W, g.H, io, qa, qb, 0, 0, s);
+        int32_t r = launch_level(p, k, g.W, g.H, io, qa, qb, 0, 0, s, 0, ar);
         if (r != DWT2_OK) return r;
     }
     return DWT2_OK;
@@ -1620,3 +1769,14 @@ const char *dwt2_error_string(int32_t code)
 const char *dwt2_version(void) { return "dwt2-b200 0.1 sm_100a (non-separable lifting, CDF 5/3)"; }
 
 }  // extern "C"
+
+namespace dwt2_detail {
+
+int32_t forward_fused_variant(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,
+                              long long out_stride, int variant, cudaStream_t s)
+{
+    return run_levels(p, in, out, count, in_stride, out_stride, 0, p->levels - 1, 0, p->geom[0].Hq, s,
+                      variant == 1 ? AR_LITERAL : AR_ADAPTED);
+}
+
+}  // namespace dwt2_detail

@@ -90,6 +90,11 @@ namespace dwt2_detail {
 // true if ptr is device (or managed) memory of the plan's device (cached)
 bool on_plan_device(const dwt2_plan *p, const void *ptr);
 
+// forward of `count` images with the literal (variant 1) or adapted (2)
+// arithmetic of the fused 5/3 kernel (dwt2.cu; schemes FUSED_LITERAL / _ADAPTED)
+int32_t forward_fused_variant(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,
+                              long long out_stride, int variant, cudaStream_t s);
+
 // inverse of all levels through the K = 2 lifting kernel (dwt97.cu)
 int32_t run_inverse_k2(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,
                        long long out_stride, cudaStream_t s);

@@ -394,6 +394,8 @@ int32_t dwt2_scheme_steps(int32_t scheme)
     case DWT2_SCHEME_NONSEP_ADAPTED: return 2;
     case DWT2_SCHEME_SEP_CONV: return 2;
     case DWT2_SCHEME_SEP_LIFTING: return 4;
+    case DWT2_SCHEME_FUSED_LITERAL: return 1;
+    case DWT2_SCHEME_FUSED_ADAPTED: return 1;
     default: return fail(DWT2_EINVAL);
     }
 }
@@ -411,6 +413,13 @@ int32_t dwt2_forward_scheme(const dwt2_plan *p, int32_t scheme, const float *in,
     const size_t out_bytes = size_t((count - 1) * out_stride + img) * sizeof(float);
     if (overlap(in, in_bytes, out, out_bytes) || !on_plan_device(p, in) || !on_plan_device(p, out))
         return fail(DWT2_EINVAL);
+    if (scheme == DWT2_SCHEME_FUSED_LITERAL || scheme == DWT2_SCHEME_FUSED_ADAPTED) {
+        int32_t r = forward_fused_variant(p, in, out, count, in_stride, out_stride,
+                                          scheme == DWT2_SCHEME_FUSED_LITERAL ? 1 : 2,
+                                          reinterpret_cast<cudaStream_t>(stream));
+        if (r == DWT2_OK) g_last_error = DWT2_OK;
+        return r;
+    }
     const bool two_buffers = scheme != DWT2_SCHEME_SEP_LIFTING && scheme != DWT2_SCHEME_NONSEP_NAIVE;
     if (two_buffers) {
         int32_t r = ensure_work(p, size_t(count) * size_t(img) * sizeof(float));

@@ -21,7 +21,7 @@ DWT2_STRIP_ALL, DWT2_STRIP_INTERIOR, DWT2_STRIP_BOUNDARY = 0, 1, 2
 DWT2_WAVELET_CDF53, DWT2_WAVELET_CDF97, DWT2_WAVELET_CDF53_K2, DWT2_WAVELET_LIFTING = 0, 1, 2, 3
 WAVELETS = {"cdf53": 0, "cdf97": 1, "cdf53_k2": 2, "lifting": 3}
 SCHEMES = {"fused": 0, "nonsep_naive": 1, "nonsep_lifting": 2, "nonsep_adapted": 3, "sep_conv": 4,
-           "sep_lifting": 5}
+           "sep_lifting": 5, "fused_literal": 6, "fused_adapted": 7}
 
 # symbol -> (restype, argtypes); mirrors include/dwt2.h exactly
 _P = ctypes.c_void_p

@@ -1,4 +1,6 @@
 """GPU parity of the paper's comparison schemes (
+the fused kernel with Eq. 5's literal operators and with Fig. 3's adapted
+arithmetic too;
 csrc/schemes.cu): separable lifting (Eq. 3, 4 kernels), separable
 convolution (Eq. 4, 2 kernels), non-separable lifting (Eq. 5, 2 kernels),
 the adapted scheme (Fig. 3, 2 kernels) and Eq. 5 as one plain kernel -- all
@@ -19,7 +21,8 @@ from tests._parity import TOL_I
 
 pytestmark = pytest.mark.gpu
 
-STEP_SCHEMES = ["nonsep_naive", "nonsep_lifting", "nonsep_adapted", "sep_conv", "sep_lifting"]
+STEP_SCHEMES = ["nonsep_naive", "nonsep_lifting", "nonsep_adapted", "sep_conv", "sep_lifting", "fused_literal",
+                "fused_adapted"]
 
 
 def run_scheme(scheme, x: np.ndarray, levels: int) -> np.ndarray:
@@ -42,7 +45,7 @@ def check(scheme, x, levels, exact, what):
 
 
 def test_steps_per_scheme():
-    assert [dwt2.dwt2_scheme_steps(dwt2.SCHEMES[s]) for s in ["fused"] + STEP_SCHEMES] == [1, 1, 2, 2, 2, 4]
+    assert [dwt2.dwt2_scheme_steps(dwt2.SCHEMES[s]) for s in ["fused"] + STEP_SCHEMES] == [1, 1, 2, 2, 2, 4, 1, 1]
     with pytest.raises(dwt2.DWT2Error):
         dwt2.dwt2_scheme_steps(99)
 
