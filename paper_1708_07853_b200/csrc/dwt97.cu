@@ -54,7 +54,10 @@ constexpr int QK = DWT2_K2_QK;             // quads per lane (2 or 4)
 constexpr int SLABQ = 32 * QK;             // quad columns per warp
 constexpr int OUTQ = 30 * QK;              // output quad columns per warp (lanes 1..30; lanes 0, 31: halo)
 constexpr int RW = 2 * SLABQ;              // floats per staged pixel row (= 64 QK)
-constexpr int DS = QK == 4 ? 6 : 8;        // raw quad rows in flight per warp (shared-memory ring, cp.async)
+#ifndef DWT2_K2_DS
+#define DWT2_K2_DS 4                      // measured: 4 > 6 > 8 > 2 (the row loop is unrolled DS times: i-cache)
+#endif
+constexpr int DS = DWT2_K2_DS;             // raw quad rows in flight per warp (shared-memory ring, cp.async)
 constexpr int DR = 1;                      // raw quad rows in flight per warp on the register path (edge slabs)
 constexpr size_t K2_SMEM = size_t(KW) * DS * 2 * RW * sizeof(float);
 static_assert(QK == 2 || QK == 4, "2 or 4 quads per lane");
@@ -531,7 +534,10 @@ __device__ __forceinline__ void cp_async8(float *dst, const float *src)
                  "l"(src) : "memory");
 }
 
-constexpr int IDSK = 8;                        // quad rows in flight per warp (inverse ring)
+#ifndef DWT2_K2INV_DS
+#define DWT2_K2INV_DS 4
+#endif
+constexpr int IDSK = DWT2_K2INV_DS;            // quad rows in flight per warp (inverse ring)
 constexpr size_t KINV_SMEM = size_t(KW) * IDSK * 4 * 64 * sizeof(float);
 
 // Interior slabs with 8-byte aligned planes stream their rows through a

@@ -273,7 +273,10 @@ __global__ void __launch_bounds__(ITHREADS, 2) dwt53_inverse_level_kernel(const 
 // holds, per plane, the window of columns [m0 - 4, m0 + 68) (18 x 16 B).
 // ---------------------------------------------------------------------------
 constexpr int IRW = 4;                         // warps per CTA (ring kernel)
-constexpr int IDS = 6;                         // quad rows in flight per warp
+#ifndef DWT2_INV_DS
+#define DWT2_INV_DS 6
+#endif
+constexpr int IDS = DWT2_INV_DS;               // quad rows in flight per warp
 constexpr int IWIN = 72;                       // window floats per plane
 constexpr int ISTAGE = 4 * IWIN;               // floats per stage
 constexpr size_t IRING_SMEM = size_t(IRW) * IDS * ISTAGE * sizeof(float);
