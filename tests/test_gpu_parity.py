@@ -296,3 +296,22 @@ def test_errors_extended_api():
         dwt2.Plan(64, 64, 1, wavelet="cdf97").forward_host(torch.zeros(64, 64).pin_memory(),
                                                            torch.zeros(64, 64).pin_memory())
     assert e.value.code == dwt2.DWT2_EUNSUPPORTED
+
+
+def test_determinism_across_runs_and_queue_orders():
+    """Pin-10: the tile queues hand tiles out in a different
+    order every run, yet every coefficient depends only on its own input
+    neighbourhood, so repeated runs -- forward, inverse, 9/7, a batch and a
+    mid-size (guided-tile) level -- are bit-identical."""
+    cases = [(8192, 4096, 1, "cdf53", 1), (4096, 4096, 3, "cdf53", 1), (2048, 2048, 2, "cdf53", 6),
+             (8192, 2048, 2, "cdf97", 1)]
+    for W, H, L, wv, n in cases:
+        x = torch.from_numpy(np.stack([workloads.uniform_real(W, H, 31 + i) for i in range(n)])).cuda()
+        x = x[0] if n == 1 else x
+        plan = dwt2.Plan(W, H, L, max_count=n, wavelet=wv)
+        y0 = plan.forward(x).clone()
+        r0 = plan.inverse(y0).clone()
+        for _ in range(3):
+            assert torch.equal(plan.forward(x), y0), (W, H, L, wv)
+            assert torch.equal(plan.inverse(y0), r0), (W, H, L, wv)
+        plan.close()
