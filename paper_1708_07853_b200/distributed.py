@@ -267,8 +267,11 @@ def strip_pyramid_step(pyr: StripPyramid, plan, overlap: bool = True, stream=Non
         pyr._launch_args, pyr._launch_key = args, key
     h = plan.handle
     out = pyr.out.data_ptr()
-    sh = (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
-    launch = dwt2.dwt2_forward_strip_level
+    if stream is not None:
+        sh = stream.cuda_stream
+    else:
+        sh = torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else 0
+    launch = getattr(plan, "launch_level", None) or dwt2.dwt2_forward_strip_level
     for k in range(pyr.levels):
         reqs = pyr.start(k) if exchange is None else exchange(k)
         bp, bpitch, lp, lpitch = pyr._launch_args[k]

@@ -194,3 +194,80 @@ def test_place_pyramid_output_tiles_global():
             D.place_pyramid_output(mark, np.ones((r1 - r0, W), np.int32), W, H, r0, r1, L)
             cover += mark
         assert (cover == 1).all(), np.argwhere(cover != 1)[:5]
+
+
+# --------------------------------------------------------------------------
+# the per-rank step of the bench (strip_pyramid_step) over gloo, with the
+# level kernels replaced by a host stand-in that checks what the real kernel
+# relies on: at every BOUNDARY launch the ghost rows hold the neighbours'
+# rows of that level's image, and the launch arguments are the level's
+# buffers.  The stand-in "produces" level k+1's owned rows (a known function
+# of the global row), so the next level's exchange moves data written by
+# the previous level's launches -- the cross-rank ordering of the step.
+# --------------------------------------------------------------------------
+
+def _level_value(k, rows, w):
+    """Synthetic content of level k's input, global rows `rows` (array), w columns."""
+    return ((rows[:, None] * 7 + np.arange(w)[None, :] * 3 + k * 101) % 1009).astype(np.float32)
+
+
+class _FakeStripPlan:
+    def __init__(self, pyr):
+        self.pyr, self.handle, self.calls = pyr, 12345, []
+
+    def launch_level(self, h, k, bp, bpitch, lp, lpitch, out, part, stream):
+        pyr = self.pyr
+        w, hgt, rb, re, gt, gb = pyr.geom[k]
+        assert h == 12345 and bp == pyr.bufs[k].data_ptr() and bpitch == pyr.bufs[k].stride(0)
+        if k + 1 < pyr.levels:
+            assert lp == pyr.owned(k + 1).data_ptr() and lpitch == pyr.owned(k + 1).stride(0)
+        if part == 2:       # BOUNDARY: ghost rows must be the neighbours' rows of this level
+            lo, hi = pyr.global_rows(k)
+            exp = _level_value(k, np.arange(lo, hi), w)
+            got = pyr.level_buffer(k).numpy()
+            assert np.array_equal(got[:gt], exp[:gt]) and np.array_equal(got[got.shape[0] - gb:], exp[exp.shape[0] - gb:])
+        self.calls.append((k, part))
+        if k + 1 < pyr.levels:      # "write" level k+1's owned rows (interior: all but first/last, boundary: those)
+            w1, h1, rb1, re1, _, _ = pyr.geom[k + 1]
+            own = pyr.owned(k + 1).numpy()
+            vals = _level_value(k + 1, np.arange(rb1, re1), w1)
+            sel = np.zeros(re1 - rb1, bool)
+            if part == 1:
+                sel[1:-1] = True
+            elif part == 2:
+                sel[0] = sel[-1] = True
+            else:
+                sel[:] = True
+            own[sel] = vals[sel]
+
+
+def _worker_step(rank, world, port, W, H, L, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pyr = D.StripPyramid(W, H, rank, world, L, device="cpu")
+        w0, h0, rb0, re0, _, _ = pyr.geom[0]
+        pyr.owned(0).copy_(torch.from_numpy(_level_value(0, np.arange(rb0, re0), w0)))
+        plan = _FakeStripPlan(pyr)
+        for _ in range(2):                      # two steps: the exchange state is reusable
+            D.strip_pyramid_step(pyr, plan, overlap=True)
+        q.put((rank, plan.calls))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,W,H,L", [(2, 48, 64, 3), (3, 30, 130, 2)])
+def test_strip_pyramid_step_gloo(world, W, H, L):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_step, args=(r, world, port, W, H, L, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, calls in res:
+        assert calls == [(k, part) for _ in range(2) for k in range(L) for part in (1, 2)]
