@@ -88,6 +88,21 @@ namespace {
 #ifndef DWT2_TPW
 #define DWT2_TPW 32                 // target tiles per warp on large levels (measured optimum)
 #endif
+#ifndef DWT2_FORCE_GENERIC                  // probes only: the generic (bulk-copy) loader everywhere
+#define DWT2_FORCE_GENERIC 0
+#endif
+#ifndef DWT2_SCALAR_LDS                    // probes only: scalar smem loads on the TMA path
+#define DWT2_SCALAR_LDS 0
+#endif
+#ifndef DWT2_GRP_NOFIX                     // probes only
+#define DWT2_GRP_NOFIX 0
+#endif
+#ifndef DWT2_NO_GRP                        // probes only: no row-grouped TMA (bulk-copy loader instead)
+#define DWT2_NO_GRP 0
+#endif
+#ifndef DWT2_FORCE_SCALAR                   // probes only: scalar subband stores everywhere
+#define DWT2_FORCE_SCALAR 0
+#endif
 #ifndef DWT2_L2_PROMOTION
 #define DWT2_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_NONE
 #endif
@@ -143,6 +158,8 @@ __device__ __forceinline__ constexpr int right_offset() { return (QPL == 2) ? 13
 // ---------------------------------------------------------------------------
 struct alignas(64) LevelArgs {
     CUtensorMap tmap;                 // 3-D {W, in_rows, count}, box {BOXW, BOXH, 1}
+                                      // (GRP: row groups {G P, flat_rows / G, 1}, box {BOXWG, ceil(BOXH / G), 1})
+    CUtensorMap tmap_b;               // GRP only: the same groups, box {BOXWG, floor(BOXH / G), 1}
     const float *in;                  // generic loader: image 0, buffer row 0
     const float *in_end;              // one past the last element of the call's input
     long long in_pitch, in_img_stride;
@@ -161,7 +178,48 @@ struct alignas(64) LevelArgs {
     int ntiles;                       // count * nblk * nslabs
     int nwarps;                       // warps in the grid
     int static_tiles;                 // 1: tile w -> warp w, no work queue
+    int glog;                         // GRP: log2 G, G = rows per 16-byte-aligned row group (2 or 4)
+    long long grp_rows;               // GRP: flat rows covered by whole groups (G floor(flat_rows / G))
+    long long flat_rows;              // GRP: count * in_rows
 };
+
+// Row-grouped TMA (GRP) for row pitches that are not a multiple of 16 bytes:
+// G consecutive rows (G = 2 if the pitch is 8 mod 16 bytes, else 4) span a
+// multiple of 16 bytes, so the input is a 2-D tensor of row GROUPS {G P
+// floats, flat_rows / G} whose row stride TMA accepts, and row r of the
+// buffer is group r / G at inner offset (r mod G) P.  A stage's BOXH rows
+// then come as G boxes, box k holding the rows r0 + k, r0 + k + G, ...; smem
+// keeps them in that order: stage row `off` lives at smem offset grp_row(off).
+// A tiled TMA load faults (illegal instruction, measured) unless its inner
+// start coordinate is 16-byte aligned, so each box starts at the column
+// aligned down from x0 - 4 and is BOXWG = BOXW + 4 wide; row class c sits
+// shifted by (c P) mod 4 floats, which the consumer adds (scalar smem loads).
+constexpr int BOXWG = BOXW + 4;
+// TMA writes each box at a 128-byte-aligned smem address, so class k starts
+// at a multiple of 32 floats: the first BOXH mod G classes hold
+// ceil(BOXH / G) rows, the others floor(BOXH / G).
+__host__ __device__ constexpr int grp_class_floats(int rows) { return (rows * BOXWG + 31) / 32 * 32; }
+__host__ __device__ constexpr int grp_stage_floats(int glog)
+{
+    return (BOXH & ((1 << glog) - 1)) * grp_class_floats((BOXH + (1 << glog) - 1) >> glog) +
+           ((1 << glog) - (BOXH & ((1 << glog) - 1))) * grp_class_floats(BOXH >> glog);
+}
+constexpr int SUBG = grp_stage_floats(1) > grp_stage_floats(2) ? grp_stage_floats(1) : grp_stage_floats(2);
+// smem offset (floats) of stage row `off` in the row-grouped layout
+template <int GG>
+__device__ __forceinline__ int grp_row(int off)
+{
+    constexpr int rem = BOXH % GG;
+    constexpr int ca = grp_class_floats((BOXH + GG - 1) / GG), cb = grp_class_floats(BOXH / GG);
+    const int k = off & (GG - 1);
+    return (k < rem ? k * ca : rem * ca + (k - rem) * cb) + (off / GG) * BOXWG;
+}
+template <bool TMA, int GG> struct RingG {
+    static constexpr int STAGE = GG > 1 ? SUBG : Ring<TMA>::STAGE;
+    static constexpr int FLOATS = S * STAGE;
+    static constexpr size_t SMEM = size_t(WARPS) * FLOATS * sizeof(float) + size_t(WARPS) * S * 8;
+};
+static_assert((SUBG * 4) % 128 == 0, "GRP stage slots must stay 128-byte aligned");
 
 // ---------------------------------------------------------------------------
 // PTX helpers (mbarrier, TMA, cp.async, PDL)
@@ -365,7 +423,7 @@ __device__ __forceinline__ RowD load_row(const float *p, int lane, const EdgeFla
 {
     float f[2 * QPL];
     const float *q = p + lane_offset<TMA>(lane);
-    if (TMA) {
+    if (TMA && !DWT2_SCALAR_LDS) {
 #pragma unroll
         for (int i = 0; i < QPL / 2; ++i) {
             const float4 t = *reinterpret_cast<const float4 *>(q + 4 * i);
@@ -666,15 +724,17 @@ __device__ __forceinline__ void storeq(float *p, const float (&x)[QPL], int n, b
 // streams tiles from the work queue through its own TMA ring (producer and
 // consumer in one warp, prefetching across tile boundaries).
 // ---------------------------------------------------------------------------
-template <bool TMA, bool VEC, int AR>
+template <bool TMA, bool VEC, int AR, int GG>
 __global__ void __launch_bounds__(THREADS, DWT2_MINB)
 dwt53_level_kernel(const __grid_constant__ LevelArgs a)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr bool GRP = GG > 1;            // row-grouped TMA, G = GG rows per group
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    float *ring = reinterpret_cast<float *>(smem_raw) + size_t(warp) * Ring<TMA>::FLOATS;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + size_t(WARPS) * Ring<TMA>::FLOATS * sizeof(float)) + warp * S;
+    float *ring = reinterpret_cast<float *>(smem_raw) + size_t(warp) * RingG<TMA, GG>::FLOATS;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + size_t(WARPS) * RingG<TMA, GG>::FLOATS * sizeof(float)) +
+                     warp * S;
 
     if (lane == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1u);     // one arrive.expect_tx per stage
@@ -683,6 +743,8 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
     __syncwarp();
     if (TMA && lane == 0)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.tmap)) : "memory");
+    if (GG > 1 && lane == 0)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.tmap_b)) : "memory");
 
     // Programmatic dependent launch: the next level may be scheduled now; it
     // waits (griddepcontrol.wait) for this grid's completion before touching
@@ -742,9 +804,42 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
             ++tq_tail;
         }
         const int slot = int(prod_seq % S);
-        float *dst = ring + slot * Ring<TMA>::STAGE;
+        float *dst = ring + slot * RingG<TMA, GG>::STAGE;
         const int r0 = tile_row0(pt) + pt_j * ROWS;
-        if (TMA) {
+        if (GRP) {
+            // G boxes per column box, one per row class (see grp_row).  Rows
+            // before the buffer or past its whole groups are zero-filled by
+            // TMA; the latter (< G rows at the very end of the buffer) are then
+            // copied by the warp once the stage has landed -- once per call.
+            constexpr int G = GG;
+            const long long fr0 = (long long)pt.img * a.in_rows + (r0 - a.in_row0);
+            if (lane == 0) {
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&bars[slot], uint32_t(NBOX * BOXH * BOXWG * sizeof(float)));
+#pragma unroll
+                for (int k = 0; k < G; ++k) {
+                    const long long fr = fr0 + k;
+                    const int g = int(fr >> (G == 2 ? 1 : 2));              // floor(fr / G), also for fr < 0
+                    const int cls = int(fr) & (G - 1);
+                    const int xk = (cls * int(a.in_pitch) + pt.x0 + BOX0) & ~3;     // 16-byte-aligned start
+                    tma_load_3d(dst + grp_row<G>(k), k < BOXH % G ? &a.tmap : &a.tmap_b, xk, g, 0, &bars[slot]);
+                }
+            }
+            if (!DWT2_GRP_NOFIX && fr0 + BOXH > a.grp_rows && fr0 < a.flat_rows) {
+                mbar_wait(&bars[slot], (prod_seq / S) & 1u);
+                for (int off = 0; off < BOXH; ++off) {
+                    const long long fr = fr0 + off;
+                    if (fr < a.grp_rows || fr >= a.flat_rows) continue;
+                    const float *src = a.in + fr * a.in_pitch;
+                    const int c0 = pt.x0 + BOX0 - ((int(fr & (G - 1)) * int(a.in_pitch)) & 3);
+                    float *d = dst + grp_row<G>(off);
+                    for (int c = lane; c < BOXWG; c += 32)
+                        if (c0 + c >= 0 && c0 + c < a.W) d[c] = src[c0 + c];
+                }
+                fence_proxy_async();       // before TMA refills this slot
+                __syncwarp();
+            }
+        } else if (TMA) {
             if (lane == 0) {
                 fence_proxy_async();
                 mbar_arrive_expect_tx(&bars[slot], uint32_t(NBOX * BOXH * BOXW * sizeof(float)));
@@ -858,7 +953,7 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
         RowD E;
         for (int j = 0; j < nst; ++j) {
             const uint32_t k = cons_seq++;
-            const float *slot = ring + int(k % S) * Ring<TMA>::STAGE;
+            const float *slot = ring + int(k % S) * RingG<TMA, GG>::STAGE;
 #ifdef DWT2_PROF
             const long long tw = clock64();
 #endif
@@ -866,8 +961,13 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
 #ifdef DWT2_PROF
             t_wait += clock64() - tw;
 #endif
+            // GRP: buffer row class of stage row 0 (the shift of row `off` is
+            // ((cls0 + off) mod G) P mod 4 floats)
+            const int cls0 = GRP ? (int)(((long long)img * a.in_rows + (r_first + j * ROWS - a.in_row0)) & (GG - 1)) : 0;
+            const int p4 = int(a.in_pitch & 3);
             auto rowp = [&](int off) -> const float * {
-                const float *p = slot + off * Lay<TMA>::RP;
+                const float *p = slot + (GRP ? grp_row<GG>(off) : off * Lay<TMA>::RP);
+                if (GRP) p += (((cls0 + off) & (GG - 1)) * p4) & 3;
                 if (!TMA) {
                     const int br = r_first + j * ROWS + off - a.in_row0;
                     if (br >= 0 && br < a.in_rows) {
@@ -879,7 +979,7 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
             };
             auto body = [&](auto edge_tag) {
                 constexpr bool EG = decltype(edge_tag)::value;
-                if (j == 0) E = load_row<TMA, EG>(rowp(0), lane, ef, true);
+                if (j == 0) E = load_row<TMA && !GRP, EG>(rowp(0), lane, ef, true);
                 const int k0 = j * PAIRS;
                 const int kend = imin(k0 + PAIRS, npairs);
                 const bool has_special_end = bottom && (kend == npairs);
@@ -887,8 +987,8 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
                     // steady state: PAIRS regular pairs, fully unrolled
 #pragma unroll
                     for (int i = 0; i < PAIRS; ++i) {
-                        const RowD O = load_row<TMA, EG>(rowp(2 * i + 1), lane, ef, false);
-                        const RowD N = load_row<TMA, EG>(rowp(2 * i + 2), lane, ef, true);
+                        const RowD O = load_row<TMA && !GRP, EG>(rowp(2 * i + 1), lane, ef, false);
+                        const RowD N = load_row<TMA && !GRP, EG>(rowp(2 * i + 2), lane, ef, true);
                         const Out o = predict_update<EG, AR>(E, O, N, cy, lane, ef, false, false);
                         storeq<VEC, EG>(pll, o.A, nL, false);
                         storeq<VEC, EG>(phl, o.B, nH, true);
@@ -906,8 +1006,8 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
                         const bool has_next = !last || (2 * n + 2 <= a.H - 1);
                         RowD O, N;
                         if (has_odd) {
-                            O = load_row<TMA, EG>(rowp(2 * i + 1), lane, ef, false);
-                            N = has_next ? load_row<TMA, EG>(rowp(2 * i + 2), lane, ef, true)
+                            O = load_row<TMA && !GRP, EG>(rowp(2 * i + 1), lane, ef, false);
+                            N = has_next ? load_row<TMA && !GRP, EG>(rowp(2 * i + 2), lane, ef, true)
                                          : E;        // even H: x[H] := x[H-2]
                         } else {
                             O = E;                   // odd H: row 2n+1 is missing
@@ -968,12 +1068,16 @@ typedef void (*KernelFn)(LevelArgs);
 template <int AR>
 KernelFn kernel_for_ar(bool tma, bool vec)
 {
-    if (tma) return vec ? dwt53_level_kernel<true, true, AR> : dwt53_level_kernel<true, false, AR>;
-    return vec ? dwt53_level_kernel<false, true, AR> : dwt53_level_kernel<false, false, AR>;
+    if (tma) return vec ? dwt53_level_kernel<true, true, AR, 1> : dwt53_level_kernel<true, false, AR, 1>;
+    return vec ? dwt53_level_kernel<false, true, AR, 1> : dwt53_level_kernel<false, false, AR, 1>;
 }
 
-KernelFn kernel_for(bool tma, bool vec, int ar = AR_GROUPED)
+// grp: the row-grouped TMA loader (product arithmetic only; the literal /
+// adapted variants keep the bulk-copy loader for such pitches)
+KernelFn kernel_for(bool tma, bool vec, int ar = AR_GROUPED, int gg = 1)
 {
+    if (gg == 2) return vec ? dwt53_level_kernel<true, true, AR_GROUPED, 2> : dwt53_level_kernel<true, false, AR_GROUPED, 2>;
+    if (gg == 4) return vec ? dwt53_level_kernel<true, true, AR_GROUPED, 4> : dwt53_level_kernel<true, false, AR_GROUPED, 4>;
     if (ar == AR_LITERAL) return kernel_for_ar<AR_LITERAL>(tma, vec);
     if (ar == AR_ADAPTED) return kernel_for_ar<AR_ADAPTED>(tma, vec);
     return kernel_for_ar<AR_GROUPED>(tma, vec);
@@ -1059,17 +1163,48 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     const long long slab_rows = (long long)io.count * a.nslabs * (lenA + lenB);
     if (slab_rows == 0) return DWT2_OK;
 
-    const bool tma = aligned(io.in, 16) && (io.in_pitch * 4) % 16 == 0 &&
+    const bool tma = !DWT2_FORCE_GENERIC && aligned(io.in, 16) && (io.in_pitch * 4) % 16 == 0 &&
                      (io.count == 1 || (io.in_img_stride * 4) % 16 == 0);
+    // other pitches: row-grouped TMA when the images are contiguous rows of
+    // one 16-byte-aligned buffer, else the bulk-copy loader
+    const int glog = (io.in_pitch % 4 == 0) ? 0 : (io.in_pitch % 2 == 0 ? 1 : 2);
+    const long long flat_rows = (long long)io.count * io.in_rows;
+    const bool grp = !tma && !DWT2_FORCE_GENERIC && !DWT2_NO_GRP && NBOX == 1 && ar == AR_GROUPED && aligned(io.in, 16) &&
+                     (io.count == 1 || io.in_img_stride == io.in_pitch * io.in_rows) &&
+                     (io.in_pitch << glog) < (1LL << 30) && (flat_rows >> glog) >= 1 &&
+                     io.in + flat_rows * io.in_pitch <= io.in_end;
     const int va = (QPL == 4) ? 16 : 8;        // subband store width in bytes
-    const bool vec = aligned(a.ll, va) && aligned(a.hl, va) && aligned(a.lh, va) && aligned(a.hh, va) &&
+    const bool vec = !DWT2_FORCE_SCALAR && aligned(a.ll, va) && aligned(a.hl, va) && aligned(a.lh, va) && aligned(a.hh, va) &&
                      io.ll_pitch % QPL == 0 && io.out_pitch % QPL == 0 &&
                      (io.count == 1 || (io.ll_img_stride % QPL == 0 && io.out_img_stride % QPL == 0));
     if (level < 0 || level >= MAX_LEVELS) return fail(DWT2_EINVAL);
     dwt2_plan::TmapCache &tc = p->tcache[level];
-    if (tma && tc.in == io.in && tc.pitch == io.in_pitch && tc.stride == io.in_img_stride && tc.W == W &&
-        tc.rows == io.in_rows && tc.count == io.count) {
+    a.glog = grp ? glog : 0;
+    a.flat_rows = flat_rows;
+    a.grp_rows = grp ? (flat_rows >> glog) << glog : 0;
+    if ((tma || grp) && tc.in == io.in && tc.pitch == io.in_pitch && tc.stride == io.in_img_stride && tc.W == W &&
+        tc.rows == io.in_rows && tc.count == io.count && tc.grp == grp) {
         a.tmap = tc.map;                      // same input tensor as the last launch of this level
+        a.tmap_b = tc.map_b;
+    } else if (grp) {
+        PFN_cuTensorMapEncodeTiled_v12000 enc = get_encode();
+        if (!enc) return fail(DWT2_ECUDA);
+        const int G = 1 << glog;
+        cuuint64_t dims[3] = {(cuuint64_t)(io.in_pitch * G), (cuuint64_t)(flat_rows >> glog), 1};
+        cuuint64_t strides[2] = {(cuuint64_t)(io.in_pitch * G * 4), (cuuint64_t)(io.in_pitch * G * 4)};
+        cuuint32_t estr[3] = {1, 1, 1};
+        for (int m = 0; m < 2; ++m) {
+            const int h = m == 0 ? (BOXH + G - 1) / G : BOXH / G;
+            cuuint32_t box[3] = {(cuuint32_t)BOXWG, (cuuint32_t)h, 1};
+            CUresult r = enc(m == 0 ? &a.tmap : &a.tmap_b, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                             const_cast<float *>(io.in), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_NONE, DWT2_L2_PROMOTION, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(DWT2_ECUDA);
+        }
+        tc.in = io.in; tc.pitch = io.in_pitch; tc.stride = io.in_img_stride;
+        tc.W = W; tc.rows = io.in_rows; tc.count = io.count; tc.grp = true;
+        tc.map = a.tmap;
+        tc.map_b = a.tmap_b;
     } else if (tma) {
         PFN_cuTensorMapEncodeTiled_v12000 enc = get_encode();
         if (!enc) return fail(DWT2_ECUDA);
@@ -1083,7 +1218,7 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
                          DWT2_L2_PROMOTION, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(DWT2_ECUDA);
         tc.in = io.in; tc.pitch = io.in_pitch; tc.stride = io.in_img_stride;
-        tc.W = W; tc.rows = io.in_rows; tc.count = io.count;
+        tc.W = W; tc.rows = io.in_rows; tc.count = io.count; tc.grp = false;
         tc.map = a.tmap;
     }
 
@@ -1092,7 +1227,7 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     // work queue (load balance).  Small levels (at most one tile per resident
     // warp): tile w goes to warp w, no queue.  tb + 1 pairs (incl. the
     // carry-in pair) fill whole stages.
-    const int max_ctas = p->max_ctas[tma ? 1 : 0];
+    const int max_ctas = p->max_ctas[tma || grp ? 1 : 0];
     const long long warps_full = (long long)max_ctas * WARPS;
     const TilePolicy &pol = tile_policy();
     long long tb = slab_rows / ((long long)pol.tpw * warps_full);
@@ -1145,14 +1280,14 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = tma ? Ring<true>::SMEM : Ring<false>::SMEM;
+    cfg.dynamicSmemBytes = grp ? RingG<true, 2>::SMEM : tma ? Ring<true>::SMEM : Ring<false>::SMEM;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel_for(tma, vec, ar), a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel_for(tma || grp, vec, ar, grp ? 1 << glog : 1), a);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(DWT2_ECUDA);
@@ -1176,6 +1311,12 @@ int32_t configure_kernels(int *max_ctas)
                     status = DWT2_ECUDA;
                     return;
                 }
+            }
+        for (int v = 0; v < 4; ++v)
+            if (cudaFuncSetAttribute(kernel_for(true, (v & 1) == 0, AR_GROUPED, v < 2 ? 2 : 4),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(RingG<true, 2>::SMEM)) != cudaSuccess) {
+                status = DWT2_ECUDA;
+                return;
             }
         int dev = 0, sms = 0, per_sm = 0;
         if (cudaGetDevice(&dev) != cudaSuccess ||

@@ -71,7 +71,8 @@ struct dwt2_plan {
         const float *in;
         long long pitch, stride;
         int W, rows, count;
-        CUtensorMap map;
+        bool grp;                           // map / map_b: row-grouped maps (dwt2.cu, GRP loader)
+        CUtensorMap map, map_b;
     };
     mutable TmapCache tcache[dwt2_detail::MAX_LEVELS];
     mutable const void *valid_ptr[4];       // device pointers already checked by on_plan_device
