@@ -84,3 +84,63 @@ def test_unaligned_base_matches(W, H):
     got = plan.forward(xin)
     assert torch.equal(got, ref)
     plan.close()
+
+
+# --------------------------------------------------------------------------
+# inverse: the unaligned ring (csrc/inverse.cu, UA: 19 chunks per plane row
+# from the 16-byte boundary below the window, per-plane row shifts)
+# --------------------------------------------------------------------------
+
+def _inverse(y, L, n=1):
+    H, W = y.shape[-2:]
+    plan = dwt2.Plan(W, H, L, max_count=n)
+    got = plan.inverse(torch.from_numpy(np.ascontiguousarray(y, dtype=np.float32)).cuda()).cpu().numpy()
+    plan.close()
+    return got
+
+
+@pytest.mark.parametrize("W", [4093, 4094, 4095, 4097, 4098, 4099])
+def test_inverse_widths_mod4(W):
+    """Random coefficients (every operand exercised), one level: bit-exact
+    against oracle(ii) for every height class."""
+    rng = np.random.default_rng(W)
+    for H in list(range(2, 10)) + [17, 64]:
+        y = rng.uniform(-300, 300, size=(H, W)).astype(np.float32)
+        got = _inverse(y, 1)
+        ref = oracle.inverse(y.astype(np.float64), 1, round_f32=True)
+        d = np.abs(got.astype(np.float64) - ref)
+        assert not d.any(), f"inverse {W}x{H}: {int(np.count_nonzero(d))} pixels off, max {d.max()}"
+
+
+@pytest.mark.parametrize("W,H,L", [(8193, 257, 4), (4094, 1027, 3), (1027, 1025, 6)])
+def test_inverse_multilevel_odd_round_trip(W, H, L):
+    """forward then inverse on the GPU, odd pitches at every level: the
+    original image within fp32 rounding of a round trip, and against oracle(ii)."""
+    x = workloads.uniform_real(W, H, W + 7 * H)
+    plan = dwt2.Plan(W, H, L)
+    xt = torch.from_numpy(x).cuda()
+    y = plan.forward(xt)
+    rec = plan.inverse(y).cpu().numpy()
+    plan.close()
+    assert np.abs(rec.astype(np.float64) - x).max() < 1e-3
+    ref = oracle.inverse(y.cpu().numpy().astype(np.float64), L, round_f32=True)
+    st = compare(rec, oracle.inverse(y.cpu().numpy().astype(np.float64), L, round_f32=False), ref, False,
+                 f"inverse {W}x{H} L{L}")
+    assert st["mismatch_ii"] == 0
+
+
+@pytest.mark.parametrize("W,H,n", [(37, 29, 5), (4095, 33, 3)])
+def test_inverse_batched_odd_and_misaligned(W, H, n):
+    """Batched odd-size pyramids (UA ring) equal the single-image results,
+    and a 4-byte-misaligned pyramid (LDG kernel) gives the same pixels."""
+    rng = np.random.default_rng(W + n)
+    ys = rng.uniform(-300, 300, size=(n, H, W)).astype(np.float32)
+    got = _inverse(ys, 2, n)
+    for i in range(n):
+        np.testing.assert_array_equal(got[i], _inverse(ys[i], 2))
+    plan = dwt2.Plan(W, H, 2)
+    buf = torch.empty(W * H + 1, device="cuda")
+    yin = buf[1:].view(H, W)
+    yin.copy_(torch.from_numpy(ys[0]))
+    np.testing.assert_array_equal(plan.inverse(yin).cpu().numpy(), got[0])
+    plan.close()
