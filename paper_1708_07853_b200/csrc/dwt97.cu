@@ -704,7 +704,10 @@ __device__ void kinv_tile(const K2InvArgs &a, float *ring, int img, int m0, int 
     if (ASYNC) cp_async_wait<0>();
 }
 
-__global__ void __launch_bounds__(KT, 4) dwt_k2_inverse_kernel(const __grid_constant__ K2InvArgs a)
+#ifndef DWT2_K2INV_MINB
+#define DWT2_K2INV_MINB 5                  // measured: 5 > 4 (config 3 +2.7 %), 6 spills
+#endif
+__global__ void __launch_bounds__(KT, DWT2_K2INV_MINB) dwt_k2_inverse_kernel(const __grid_constant__ K2InvArgs a)
 {
     extern __shared__ __align__(16) float kinv_smem[];
     pdl_launch97();

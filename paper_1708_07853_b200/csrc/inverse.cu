@@ -273,8 +273,11 @@ __global__ void __launch_bounds__(ITHREADS, 2) dwt53_inverse_level_kernel(const 
 // holds, per plane, the window of columns [m0 - 4, m0 + 68) (18 x 16 B).
 // ---------------------------------------------------------------------------
 constexpr int IRW = 4;                         // warps per CTA (ring kernel)
+#ifndef DWT2_INV_MINB
+#define DWT2_INV_MINB 4                        // resident CTAs per SM the register budget aims at
+#endif
 #ifndef DWT2_INV_DS
-#define DWT2_INV_DS 6
+#define DWT2_INV_DS 4                          // measured with 4 CTAs per SM: 4 rows in flight > 3, 5 (> 6 at 3 CTAs)
 #endif
 constexpr int IDS = DWT2_INV_DS;               // quad rows in flight per warp
 constexpr int IWIN = 72;                       // window floats per plane
@@ -424,7 +427,7 @@ __device__ __forceinline__ void ring_tile(const InvArgs &a, float *ring, int img
     if (n1 == Hq) undo_predict_store<true, EDGE>(a, prev, prev, img, n1 - 1, m0, lane, (a.H & 1) == 0);
 }
 
-__global__ void __launch_bounds__(IRW * 32, 3) dwt53_inverse_ring_kernel(const __grid_constant__ InvArgs a)
+__global__ void __launch_bounds__(IRW * 32, DWT2_INV_MINB) dwt53_inverse_ring_kernel(const __grid_constant__ InvArgs a)
 {
     extern __shared__ __align__(16) float iring_smem[];
     pdl_launch_inv();
