@@ -590,8 +590,9 @@ def main():
     k_bytes = runner.level1_bytes
     achieved = k_bytes / (k_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
-    traffic = ncu_traffic(cfg.name if args.wavelet == "cdf53" else f"{cfg.name}_{args.wavelet}") \
-        if world == 1 and args.op == "forward" and args.scheme == "fused" else None
+    # key of the committed ncu capture: config [+ _cdf97] [+ _inverse]
+    tkey = cfg.name + ("" if args.wavelet == "cdf53" else f"_{args.wavelet}") + ("_inverse" if args.op == "inverse" else "")
+    traffic = ncu_traffic(tkey) if world == 1 and args.scheme == "fused" else None
 
     # end to end through the host-buffer API
     e2e = None
