@@ -5,7 +5,9 @@
 // (predict, then update) and its single in-level synchronisation point `|`
 // map onto one pass over HBM:
 //
-//   HBM --TMA--> per-warp smem ring (136-column slab + halo, R rows/stage)
+//   HBM --TMA--> per-warp smem ring (136-column slab + halo, R rows/stage;
+//                row pitches that are not a multiple of 16 bytes: row-grouped
+//                tensor maps, see grp_row)
 //       --LDS.128--> registers: spatial predict (Eq. (5) right factor)
 //       --warp shuffle (m-1 neighbour) + register carry (n-1 neighbour)-->
 //       spatial update (Eq. (5) left factor) --> 4 subband stores (STG.64)
@@ -848,7 +850,9 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
                     tma_load_3d(dst + Lay<TMA>::SUB, &a.tmap, pt.x0 + BOX1, r0 - a.in_row0, pt.img, &bars[slot]);
             }
         } else {
-            // Unaligned rows (odd widths, e.g. config 5's 4095-wide images):
+            // Unaligned rows the row-grouped loader does not take (a base
+            // pointer that is not 16-byte aligned, batched images with gaps,
+            // the literal / adapted arithmetic variants):
             // one 1-D bulk copy per box row (cp.async.bulk, 16-byte granules)
             // of the 140 floats from the row's 16-byte-aligned address at or
             // below column x0 + BOX0 (the consumer re-derives the shift).  Lane
