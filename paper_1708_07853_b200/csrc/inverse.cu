@@ -58,6 +58,8 @@ struct InvArgs {
     long long out_pitch, out_img;
     int W, H;                              // reconstructed size
     int nslabs, nblk, tb, count;
+    int nblk_a, tb_b, split;               // ring kernel, guided tiles: blocks < nblk_a are tb rows from 0,
+                                           // the rest tb_b rows from quad row `split` (nblk_a = nblk: uniform)
     long long ntiles;
     const float *ll_lo, *ll_hi, *d_lo, *d_hi;   // allocation ranges of the LL / detail sources (ring loader)
     unsigned int *counter;                       // tile queue (queue.cuh)
@@ -443,7 +445,8 @@ __global__ void __launch_bounds__(IRW * 32, DWT2_INV_MINB) dwt53_inverse_ring_ke
         const int blk = r / a.nslabs;
         const int slab = r - blk * a.nslabs;
         const int m0 = slab * IQ;
-        const int n0 = blk * a.tb, n1 = min(n0 + a.tb, Hq);
+        const int n0 = blk < a.nblk_a ? blk * a.tb : a.split + (blk - a.nblk_a) * a.tb_b;
+        const int n1 = min(n0 + (blk < a.nblk_a ? a.tb : a.tb_b), blk < a.nblk_a ? min(a.split, Hq) : Hq);
         // interior: every plane's window [m0 - 4, m0 + 68) lies inside its row
         // (the narrowest planes, HL / HH, are Wh wide), so no clamping and no
         // range check of the cp.async sources
@@ -506,6 +509,27 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
         tb = std::max<long long>(8, std::min<long long>(256, tb));
         a.tb = int(tb);
         a.nblk = int((Hq + tb - 1) / tb);
+        a.nblk_a = a.nblk;
+        a.split = Hq;
+        a.tb_b = a.tb;
+        // guided tiles on mid-size levels (few tiles per warp): one large tile
+        // per warp over ~70 % of the rows, then ~4 small tiles per warp (as
+        // the forward kernel, dwt2.cu)
+        static const int guided = [] { const char *v = getenv("DWT2_INV_GUIDED"); return !(v && v[0] == '0'); }();
+        if (guided && a.count == 1 && slab_rows < 256 * rwarps && slab_rows >= 8 * rwarps) {
+            const long long nba = std::max<long long>(1, rwarps / a.nslabs);
+            const long long tba = (7 * Hq / 10) / nba;
+            if (tba >= 16) {
+                a.tb = int(tba);
+                a.nblk_a = int(nba);
+                a.split = int(nba * tba);
+                const long long rest = Hq - a.split;
+                long long tbb = rest * a.nslabs / (4 * rwarps);
+                tbb = std::max<long long>(8, std::min<long long>(256, tbb));
+                a.tb_b = int(tbb);
+                a.nblk = a.nblk_a + int((rest + tbb - 1) / tbb);
+            }
+        }
         a.ntiles = (long long)a.count * a.nblk * a.nslabs;
         const long long want = (a.ntiles + IRW - 1) / IRW;
         const int grid = int(std::max<long long>(1, std::min<long long>(want, rwarps / IRW)));
@@ -535,6 +559,9 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
     tb = std::max<long long>(8, std::min<long long>(256, tb));
     a.tb = int(tb);
     a.nblk = int((Hq + tb - 1) / tb);
+    a.nblk_a = a.nblk;
+    a.split = Hq;
+    a.tb_b = a.tb;
     a.ntiles = (long long)a.count * a.nblk * a.nslabs;
     const long long want = (a.ntiles + IWARPS - 1) / IWARPS;
     const int grid = int(std::max<long long>(1, std::min<long long>(want, warps / IWARPS)));
