@@ -1280,8 +1280,7 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     a.static_tiles = ntiles <= a.nwarps ? 1 : 0;
     a.counter = p->counters + 2 * ((queue ? QUEUE_STRIP_BOUNDARY : QUEUE_FORWARD) + level);
 
-    cudaLaunchConfig_t cfg;
-    memset(&cfg, 0, sizeof(cfg));
+    cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = grp ? RingG<true, 2>::SMEM : tma ? Ring<true>::SMEM : Ring<false>::SMEM;

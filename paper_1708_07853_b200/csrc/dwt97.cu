@@ -440,8 +440,7 @@ int32_t launch_k2_level(const dwt2_plan *p, K2Args a, cudaStream_t s)
                      aligned(a.ll, 4 * QK) && aligned(a.hl, 4 * QK) && aligned(a.lh, 4 * QK) && aligned(a.hh, 4 * QK) &&
                      a.ll_pitch % QK == 0 && a.out_pitch % QK == 0 &&
                      (a.count == 1 || (a.ll_img % QK == 0 && a.out_img % QK == 0));
-    cudaLaunchConfig_t cfg;
-    memset(&cfg, 0, sizeof(cfg));
+    cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(KT);
     cfg.dynamicSmemBytes = K2_SMEM;
@@ -759,8 +758,7 @@ int32_t launch_k2_inverse_level(const dwt2_plan *p, K2InvArgs a, cudaStream_t s)
     const long long want = (a.ntiles + KW - 1) / KW;
     const int grid = int(std::max<long long>(1, std::min<long long>(want, warps / KW)));
     a.nwarps = grid * KW;
-    cudaLaunchConfig_t cfg;
-    memset(&cfg, 0, sizeof(cfg));
+    cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(KT);
     cfg.dynamicSmemBytes = KINV_SMEM;

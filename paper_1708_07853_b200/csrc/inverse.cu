@@ -534,8 +534,7 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
         const long long want = (a.ntiles + IRW - 1) / IRW;
         const int grid = int(std::max<long long>(1, std::min<long long>(want, rwarps / IRW)));
         a.nwarps = grid * IRW;
-        cudaLaunchConfig_t cfg;
-        memset(&cfg, 0, sizeof(cfg));
+        cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(IRW * 32);
         cfg.dynamicSmemBytes = IRING_SMEM;
@@ -569,8 +568,7 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
     const bool vec = aligned(a.ll, 8) && aligned(a.hl, 8) && aligned(a.lh, 8) && aligned(a.hh, 8) &&
                      a.ll_pitch % 2 == 0 && a.d_pitch % 2 == 0 && (a.count == 1 || (a.ll_img % 2 == 0 && a.d_img % 2 == 0)) &&
                      aligned(a.out, 16) && a.out_pitch % 4 == 0 && (a.count == 1 || a.out_img % 4 == 0);
-    cudaLaunchConfig_t cfg;
-    memset(&cfg, 0, sizeof(cfg));
+    cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(ITHREADS);
     cfg.stream = s;
