@@ -1115,6 +1115,8 @@ struct TilePolicy {
     int guided;    // mid-size levels: large tiles first, small ones last (DWT2_GUIDED=0 disables)
     int guided_a;  // percent of the rows in the large (one per warp) tiles
     int guided_b;  // small tiles per warp for the rest
+    int tb_large;  // tile height of large levels (0: off)
+    int large_tpw; // a level is large from this many tiles per warp at tb_large
 };
 
 const TilePolicy &tile_policy()
@@ -1133,6 +1135,9 @@ const TilePolicy &tile_policy()
         pol.guided = (g && g[0] == '0') ? 0 : 1;
         pol.guided_a = env("DWT2_GUIDED_A", 70);
         pol.guided_b = env("DWT2_GUIDED_B", 4);
+        const char *tl = getenv("DWT2_TB_LARGE");
+        pol.tb_large = tl ? atoi(tl) : 15;
+        pol.large_tpw = env("DWT2_LARGE_TPW", 9);
     });
     return pol;
 }
@@ -1235,6 +1240,15 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     const long long warps_full = (long long)max_ctas * WARPS;
     const TilePolicy &pol = tile_policy();
     long long tb = slab_rows / ((long long)pol.tpw * warps_full);
+    if (pol.tb_large > 0 && slab_rows >= (long long)pol.large_tpw * pol.tb_large * warps_full) {
+        // large levels (>= large_tpw tiles per warp at tb_large quad rows):
+        // tb_large, measured best from 16384 x 6144 up -- 16384 x 8192 (a
+        // config-3 strip at G = 2): 0.82 -> 0.96 of copy against 11-row
+        // tiles; config 5's batch: 571 -> 602 Gpix/s against 55-row ones;
+        // 16384^2 unchanged (tpw already gave 15).  Smaller levels keep the
+        // rules below (8192^2: 11-row tiles 0.93, 15-row 0.88).
+        tb = pol.tb_large;
+    }
     if (tb < pol.min_tb) {
         // fewer than tpw tiles per warp even at the minimum tile height: keep
         // the minimum height (queue balancing) while that still gives every
