@@ -507,6 +507,12 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
         const int tpw = env_tpw > 0 ? env_tpw : (slab_rows >= 256 * rwarps ? 16 : 4);
         long long tb = slab_rows / (tpw * rwarps);
         tb = std::max<long long>(8, std::min<long long>(256, tb));
+        // levels with >= 64 quad rows per warp: 20-row tiles (measured over
+        // 8192^2 .. 16384^2 against 8, 12, 16, 24, 27..55-row tiles and the
+        // guided split: 16384 x 8192 0.80 -> 0.88, 16384^2 0.89 -> 0.91,
+        // 8192^2 0.81 -> 0.83 of copy); guided tiles below 64 rows per warp
+        static const int env_tb = [] { const char *v = getenv("DWT2_INV_TB"); return v ? atoi(v) : 20; }();
+        if (env_tpw <= 0 && env_tb > 0 && slab_rows >= 64 * rwarps) tb = env_tb;
         a.tb = int(tb);
         a.nblk = int((Hq + tb - 1) / tb);
         a.nblk_a = a.nblk;
@@ -516,7 +522,7 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
         // per warp over ~70 % of the rows, then ~4 small tiles per warp (as
         // the forward kernel, dwt2.cu)
         static const int guided = [] { const char *v = getenv("DWT2_INV_GUIDED"); return !(v && v[0] == '0'); }();
-        if (guided && a.count == 1 && slab_rows < 256 * rwarps && slab_rows >= 8 * rwarps) {
+        if (guided && a.count == 1 && slab_rows < 64 * rwarps && slab_rows >= 8 * rwarps) {
             const long long nba = std::max<long long>(1, rwarps / a.nslabs);
             const long long tba = (7 * Hq / 10) / nba;
             if (tba >= 16) {

@@ -1,5 +1,7 @@
 """Level-1 time of W x H images under the tile policy's environment knobs
-(DWT2_TPW, DWT2_MIN_TB, ...): python scripts/tile_probe.py W H [W H ...]."""
+(DWT2_TPW, DWT2_MIN_TB, ...): python scripts/tile_probe.py W H [W H ...].
+PROBE_OP=inverse times the inverse, PROBE_WAVELET=cdf97 the K = 2 kernels."""
+import os
 import sys
 
 import torch
@@ -15,8 +17,12 @@ out = []
 for W, H in zip(a[0::2], a[1::2]):
     x = torch.from_numpy(workloads.uniform_int(W, H, 1)).cuda()
     y = torch.empty_like(x)
-    p = dwt2.Plan(W, H, 1)
-    us = time_calls(lambda q: p.forward(q[0], q[1]), [(x, y)], 10)
+    p = dwt2.Plan(W, H, 1, wavelet=os.environ.get("PROBE_WAVELET", "cdf53"))
+    if os.environ.get("PROBE_OP") == "inverse":
+        x = p.forward(x).clone()
+        us = time_calls(lambda q: p.inverse(q[0], q[1]), [(x, y)], 10)
+    else:
+        us = time_calls(lambda q: p.forward(q[0], q[1]), [(x, y)], 10)
     out.append(f"{W}x{H} {us:.1f} us ({8 * W * H / us / 1e3 / 6535:.3f})")
     p.close()
 print(" | ".join(out))
