@@ -131,6 +131,18 @@ def test_config3_16384_sampled():
     assert np.abs(got).max() <= 1020
 
 
+@pytest.mark.parametrize("W,H", [(16384, 8192), (20000, 6001), (20001, 6001)])
+def test_large_level_tiles_sampled(W, H):
+    """Levels large enough for the 15-row tile rule (tile_policy: >= 9 tiles
+    per warp), incl. an odd height and a width that is not a slab multiple:
+    border quads and 200k random positions against the pointwise oracle."""
+    x = workloads.uniform_int(W, H, W + H)
+    got = gpu_forward(x, 1)
+    rng = np.random.default_rng(W)
+    b, m, n = sample_positions(W, H, 200_000, rng)
+    np.testing.assert_array_equal(gather(got, W, H, b, m, n).astype(np.float64), oracle.conv_sample(x, b, m, n))
+
+
 def test_config5_batch_sampled():
     """Config 5 through dwt2_forward_batched (one launch per level over the
     group): 12 of each image size checked in full against the oracle (3
