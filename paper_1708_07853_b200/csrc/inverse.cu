@@ -560,7 +560,8 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
     // tile height: ~8 tiles per resident warp, at least 8 quad rows (the
     // halo row re-read costs 1 / tb), at most 256
     long long slab_rows = (long long)a.count * a.nslabs * Hq;
-    long long tb = slab_rows / (8 * warps);
+    static const int ldg_tpw = [] { const char *v = getenv("DWT2_INV_LDG_TPW"); return v && atoi(v) > 0 ? atoi(v) : 8; }();
+    long long tb = slab_rows / (ldg_tpw * warps);
     tb = std::max<long long>(8, std::min<long long>(256, tb));
     a.tb = int(tb);
     a.nblk = int((Hq + tb - 1) / tb);
