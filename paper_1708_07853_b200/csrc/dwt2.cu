@@ -751,13 +751,17 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
     // Programmatic dependent launch: the next level may be scheduled now; it
     // waits (griddepcontrol.wait) for this grid's completion before touching
     // memory, exactly as this grid waits for its predecessor here.
+#ifdef DWT2_PROF
+    const unsigned long long t_entry = gtimer();
+#endif
     pdl_launch_dependents();
     pdl_wait();
 #ifdef DWT2_PROF
     if (threadIdx.x == 0 && blockIdx.x < 4096) {
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        g_cta[blockIdx.x][0] = gtimer();
+        g_cta[blockIdx.x][0] = t_entry;
+        g_cta[blockIdx.x][1] = gtimer();
         g_cta[blockIdx.x][3] = smid;
     }
     const long long t_work = clock64();
@@ -1275,7 +1279,8 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
         if (tb_a >= 2 * PAIRS - 1) {
             const long long rows_a = nblk_a * tb_a, rest = lenA - rows_a;
             long long tb_b = rest * a.nslabs / ((long long)pol.guided_b * warps_full);
-            tb_b = std::max<long long>(2 * PAIRS - 1, (tb_b + 1 + PAIRS - 1) / PAIRS * PAIRS - 1);
+            static const int min_b = [] { const char *v = getenv("DWT2_GUIDED_MINB"); return v && atoi(v) > 0 ? atoi(v) : 2; }();
+            tb_b = std::max<long long>(min_b * PAIRS - 1, (tb_b + 1 + PAIRS - 1) / PAIRS * PAIRS - 1);
             a.tb = int(tb_a);
             a.tb_b = int(std::min<long long>(tb_b, MAX_TILE_ROWS));
             a.qa1 = int(qa0 + rows_a);

@@ -3,7 +3,8 @@ import ctypes, sys
 import numpy as np, torch
 sys.path.insert(0, '.')
 from paper_1708_07853_b200 import dwt2, workloads
-W = H = 16384
+W = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+H = int(sys.argv[2]) if len(sys.argv) > 2 else W
 x = torch.from_numpy(workloads.uniform_int(W, H, 3)).cuda()
 out = torch.empty_like(x)
 p = dwt2.Plan(W, H, 1)
