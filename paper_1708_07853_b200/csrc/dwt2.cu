@@ -158,6 +158,31 @@ __device__ __forceinline__ constexpr int right_offset() { return (QPL == 2) ? 13
 // Kernel arguments (a __grid_constant__ parameter: the TMA descriptor must be
 // 64-byte aligned and live in param space)
 // ---------------------------------------------------------------------------
+// Division by a launch-constant divisor without the integer-divide sequence
+// (decode_tile runs twice per tile; ncu had its two divisions at 3.5 % of the
+// kernel's instructions): q = (umulhi(n, mul) + n) >> shift for n < 2^31
+// (Granlund & Montgomery's round-up multiplier; d = 1: mul = shift = 0).
+struct FastDiv {
+    unsigned mul, shift;
+};
+
+inline FastDiv make_fastdiv(unsigned d)
+{
+    FastDiv f{0u, 0u};
+    if (d > 1) {
+        unsigned sh = 0;
+        while ((1ull << sh) < d) ++sh;
+        f.shift = sh;
+        f.mul = unsigned(((1ull << 32) * ((1ull << sh) - d)) / d + 1);
+    }
+    return f;
+}
+
+__device__ __forceinline__ int fdiv(int n, FastDiv f)
+{
+    return int((__umulhi(unsigned(n), f.mul) + unsigned(n)) >> f.shift);
+}
+
 struct alignas(64) LevelArgs {
     CUtensorMap tmap;                 // 3-D {W, in_rows, count}, box {BOXW, BOXH, 1}
                                       // (GRP: row groups {G P, flat_rows / G, 1}, box {BOXWG, ceil(BOXH / G), 1})
@@ -173,6 +198,8 @@ struct alignas(64) LevelArgs {
     int in_row0, in_rows;             // global row of buffer row 0; rows present in the buffer
     int out_q0;                       // global quad row stored at output row 0
     int nslabs, count;
+    FastDiv fd_slabs, fd_img;         // division by nslabs and by nblk * nslabs
+    int unroll_first;                 // 1: a tile's first stage (carry-in pair) on the unrolled path
     int qa0, qa1, qb0, qb1;           // quad-row ranges [qa0, qa1) and [qb0, qb1)
     int tb;                           // quad rows per tile (range A)
     int tb_b;                         // quad rows per tile (range B)
@@ -349,9 +376,9 @@ __device__ __forceinline__ Tile decode_tile(const LevelArgs &a, int t)
 {
     Tile T;
     const int per_img = a.nblk * a.nslabs;
-    T.img = t / per_img;
+    T.img = fdiv(t, a.fd_img);
     const int r = t - T.img * per_img;
-    const int blk = r / a.nslabs;
+    const int blk = fdiv(r, a.fd_slabs);
     const int slab = r - blk * a.nslabs;
     T.x0 = slab * SLAB;
     if (blk < a.nblk_a) {
@@ -991,13 +1018,21 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
                 const int k0 = j * PAIRS;
                 const int kend = imin(k0 + PAIRS, npairs);
                 const bool has_special_end = bottom && (kend == npairs);
-                if (j > 0 && kend - k0 == PAIRS && !has_special_end) {
-                    // steady state: PAIRS regular pairs, fully unrolled
+                if ((j > 0 || (!top && a.unroll_first)) && kend - k0 == PAIRS && !has_special_end) {
+                    // steady state: PAIRS regular pairs, fully unrolled; the first
+                    // stage of a tile below the top starts with its carry-in pair
+                    // (quad row qa - 1: carries only, nothing stored)
+                    const bool cin0 = (j == 0);
 #pragma unroll
                     for (int i = 0; i < PAIRS; ++i) {
                         const RowD O = load_row<TMA && !GRP, EG>(rowp(2 * i + 1), lane, ef, false);
                         const RowD N = load_row<TMA && !GRP, EG>(rowp(2 * i + 2), lane, ef, true);
-                        const Out o = predict_update<EG, AR>(E, O, N, cy, lane, ef, false, false);
+                        const bool cin = (i == 0) && cin0;
+                        const Out o = predict_update<EG, AR>(E, O, N, cy, lane, ef, cin, false);
+                        if (cin) {
+                            E = N;
+                            continue;
+                        }
                         storeq<VEC, EG>(pll, o.A, nL, false);
                         storeq<VEC, EG>(phl, o.B, nH, true);
                         storeq<VEC, EG>(plh, o.C, nL, true);
@@ -1293,10 +1328,20 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     const long long ntiles = (long long)io.count * a.nblk * a.nslabs;
     if (ntiles >= (1LL << 31)) return fail(DWT2_EINVAL);
     a.ntiles = int(ntiles);
+    a.fd_slabs = make_fastdiv(unsigned(a.nslabs));
+    a.fd_img = make_fastdiv(unsigned(a.nblk * a.nslabs));
     const long long want_ctas = (ntiles + WARPS - 1) / WARPS;
     const int grid = int(std::max<long long>(1, std::min<long long>(max_ctas, want_ctas)));
     a.nwarps = grid * WARPS;
     a.static_tiles = ntiles <= a.nwarps ? 1 : 0;
+    // the first stage of a tile on the unrolled path: measured faster on
+    // guided (mid-size) levels, one-tile-per-warp levels and on the
+    // row-grouped loader (4096^2 0.79 -> 0.85, 16384 x 2048 0.85 -> 0.87,
+    // 2048^2 0.55 -> 0.60, 8193^2 0.85 -> 0.87, 4095 x 3001 0.60 -> 0.68) but
+    // slower on large 3-D TMA levels (8192^2 0.94 -> 0.83, 16384^2 0.98 ->
+    // 0.97), for reasons not established; DWT2_UNROLL_FIRST=0/1 forces it
+    static const int env_uf = [] { const char *v = getenv("DWT2_UNROLL_FIRST"); return v ? atoi(v) : -1; }();
+    a.unroll_first = env_uf >= 0 ? env_uf : ((a.tb_b != a.tb || a.qb1 > a.qb0 || grp || a.static_tiles) ? 1 : 0);
     a.counter = p->counters + 2 * ((queue ? QUEUE_STRIP_BOUNDARY : QUEUE_FORWARD) + level);
 
     cudaLaunchConfig_t cfg = {};
