@@ -44,5 +44,10 @@ def time_calls(call, pairs, K, reps=3):
 
 
 def n_pairs(bytes_per_call, K):
-    """Distinct buffer pairs needed so that no timed call finds its input in L2."""
-    return K if bytes_per_call < 2 * L2_BYTES else 1
+    """Buffer pairs cycled so that no timed call finds its input in L2: a pair
+    is reused only after more than 2x L2 of other traffic, or (small calls)
+    each of the K calls gets its own pair, read once after the flush
+    (bench.py's buffer_pairs)."""
+    if bytes_per_call >= 2 * L2_BYTES:
+        return 1
+    return min(K, int(-(-2 * L2_BYTES // bytes_per_call)) + 1)

@@ -1,6 +1,7 @@
 """Level-1 time of W x H images under the tile policy's environment knobs
 (DWT2_TPW, DWT2_MIN_TB, ...): python scripts/tile_probe.py W H [W H ...].
-PROBE_OP=inverse times the inverse, PROBE_WAVELET=cdf97 the K = 2 kernels."""
+PROBE_OP=inverse times the inverse, PROBE_WAVELET=cdf97 the K = 2 kernels,
+PROBE_COLD=1 gives every call its own buffers (forward only) as bench.py does."""
 import os
 import sys
 
@@ -8,7 +9,7 @@ import torch
 
 sys.path.insert(0, ".")
 sys.path.insert(0, "scripts")
-from _timing import time_calls  # noqa: E402
+from _timing import n_pairs, time_calls  # noqa: E402
 from paper_1708_07853_b200 import dwt2, workloads  # noqa: E402
 
 torch.cuda.set_device(0)
@@ -22,7 +23,10 @@ for W, H in zip(a[0::2], a[1::2]):
         x = p.forward(x).clone()
         us = time_calls(lambda q: p.inverse(q[0], q[1]), [(x, y)], 10)
     else:
-        us = time_calls(lambda q: p.forward(q[0], q[1]), [(x, y)], 10)
+        pairs = [(x, y)]
+    if os.environ.get("PROBE_COLD"):      # the bench's protocol: one buffer pair per call below 2x L2
+        pairs += [(x.clone(), torch.empty_like(y)) for _ in range(n_pairs(8 * W * H, 10) - 1)]
+    us = time_calls(lambda q: p.forward(q[0], q[1]), pairs, 10)
     out.append(f"{W}x{H} {us:.1f} us ({8 * W * H / us / 1e3 / 6535:.3f})")
     p.close()
 print(" | ".join(out))
