@@ -158,31 +158,6 @@ __device__ __forceinline__ constexpr int right_offset() { return (QPL == 2) ? 13
 // Kernel arguments (a __grid_constant__ parameter: the TMA descriptor must be
 // 64-byte aligned and live in param space)
 // ---------------------------------------------------------------------------
-// Division by a launch-constant divisor without the integer-divide sequence
-// (decode_tile runs twice per tile; ncu had its two divisions at 3.5 % of the
-// kernel's instructions): q = (umulhi(n, mul) + n) >> shift for n < 2^31
-// (Granlund & Montgomery's round-up multiplier; d = 1: mul = shift = 0).
-struct FastDiv {
-    unsigned mul, shift;
-};
-
-inline FastDiv make_fastdiv(unsigned d)
-{
-    FastDiv f{0u, 0u};
-    if (d > 1) {
-        unsigned sh = 0;
-        while ((1ull << sh) < d) ++sh;
-        f.shift = sh;
-        f.mul = unsigned(((1ull << 32) * ((1ull << sh) - d)) / d + 1);
-    }
-    return f;
-}
-
-__device__ __forceinline__ int fdiv(int n, FastDiv f)
-{
-    return int((__umulhi(unsigned(n), f.mul) + unsigned(n)) >> f.shift);
-}
-
 struct alignas(64) LevelArgs {
     CUtensorMap tmap;                 // 3-D {W, in_rows, count}, box {BOXW, BOXH, 1}
                                       // (GRP: row groups {G P, flat_rows / G, 1}, box {BOXWG, ceil(BOXH / G), 1})

@@ -22,6 +22,31 @@ constexpr int QUEUE_STRIP_BOUNDARY = MAX_LEVELS;  // strip BOUNDARY launches (ma
 constexpr int QUEUE_INVERSE = 2 * MAX_LEVELS;     // inverse level kernels
 constexpr int QUEUE_SLOTS = 3 * MAX_LEVELS;
 
+// Division by a launch-constant divisor without the integer-divide sequence
+// (decode_tile runs twice per tile; ncu had its two divisions at 3.5 % of the
+// kernel's instructions): q = (umulhi(n, mul) + n) >> shift for n < 2^31
+// (Granlund & Montgomery's round-up multiplier; d = 1: mul = shift = 0).
+struct FastDiv {
+    unsigned mul, shift;
+};
+
+inline FastDiv make_fastdiv(unsigned d)
+{
+    FastDiv f{0u, 0u};
+    if (d > 1) {
+        unsigned sh = 0;
+        while ((1ull << sh) < d) ++sh;
+        f.shift = sh;
+        f.mul = unsigned(((1ull << 32) * ((1ull << sh) - d)) / d + 1);
+    }
+    return f;
+}
+
+__device__ __forceinline__ int fdiv(int n, FastDiv f)
+{
+    return int((__umulhi(unsigned(n), f.mul) + unsigned(n)) >> f.shift);
+}
+
 struct LevelGeom {
     int W, H;            // level input size
     int Wq, Hq;          // LL size: ceil(W / 2) x ceil(H / 2)

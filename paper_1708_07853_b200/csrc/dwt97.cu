@@ -81,6 +81,7 @@ struct K2Args {
     int W, H;
     int nslabs, tb, nblk, count;
     long long ntiles;
+    FastDiv fd_img, fd_slabs;              // division by nblk * nslabs and by nslabs (ntiles < 2^31)
     double c0, c1, c2, c3;                 // lifting coefficients (predict, update, predict, update)
     double sll, sd, shh;                   // output scaling: LL, HL / LH, HH
     unsigned int *counter;                 // tile queue (queue.cuh)
@@ -372,9 +373,9 @@ __global__ void __launch_bounds__(KT, DWT2_K2_MINB) dwt_k2_level_kernel(const __
     const long long per_img = (long long)a.nblk * a.nslabs;
     for (long long t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane); t < a.ntiles;
          t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane)) {
-        const int img = int(t / per_img);
+        const int img = fdiv(int(t), a.fd_img);
         const int rr = int(t - img * per_img);
-        const int blk = rr / a.nslabs;
+        const int blk = fdiv(rr, a.fd_slabs);
         const int slab = rr - blk * a.nslabs;
         const int m0 = slab * OUTQ;
         const int n0 = blk * a.tb, n1 = min(n0 + a.tb, Hq);
@@ -435,6 +436,9 @@ int32_t launch_k2_level(const dwt2_plan *p, K2Args a, cudaStream_t s)
     a.tb = int(tb);
     a.nblk = int((Hq + tb - 1) / tb);
     a.ntiles = (long long)a.count * a.nblk * a.nslabs;
+    a.fd_img = make_fastdiv(unsigned(a.nblk * a.nslabs));
+    a.fd_slabs = make_fastdiv(unsigned(a.nslabs));
+    if (a.ntiles >= (1LL << 31)) return fail(DWT2_EINVAL);
     const long long want = (a.ntiles + KW - 1) / KW;
     const int grid = int(std::max<long long>(1, std::min<long long>(want, warps / KW)));
     a.nwarps = grid * KW;
@@ -489,6 +493,7 @@ struct K2InvArgs {
     int W, H;
     int nslabs, tb, nblk, count;
     long long ntiles;
+    FastDiv fd_img, fd_slabs;              // division by nblk * nslabs and by nslabs (ntiles < 2^31)
     double c0, c1, c2, c3, K2sq, invK2sq;  // K^2 and 1 / K^2
     int async;                             // 1: every plane 8-byte aligned with even pitches (cp.async ring)
     int vec_out;                           // 1: output 16-byte aligned with pitch % 4 == 0 (float4 stores)
@@ -719,9 +724,9 @@ __global__ void __launch_bounds__(KT, DWT2_K2INV_MINB) dwt_k2_inverse_kernel(con
     const long long per_img = (long long)a.nblk * a.nslabs;
     for (long long t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane); t < a.ntiles;
          t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane)) {
-        const int img = int(t / per_img);
+        const int img = fdiv(int(t), a.fd_img);
         const int rr = int(t - img * per_img);
-        const int blk = rr / a.nslabs;
+        const int blk = fdiv(rr, a.fd_slabs);
         const int slab = rr - blk * a.nslabs;
         const int m0 = slab * OUTQ;
         const int n0 = blk * a.tb, n1 = min(n0 + a.tb, Hq);
@@ -763,6 +768,9 @@ int32_t launch_k2_inverse_level(const dwt2_plan *p, K2InvArgs a, cudaStream_t s)
     a.tb = int(tb);
     a.nblk = int((Hq + tb - 1) / tb);
     a.ntiles = (long long)a.count * a.nblk * a.nslabs;
+    a.fd_img = make_fastdiv(unsigned(a.nblk * a.nslabs));
+    a.fd_slabs = make_fastdiv(unsigned(a.nslabs));
+    if (a.ntiles >= (1LL << 31)) return fail(DWT2_EINVAL);
     const long long want = (a.ntiles + KW - 1) / KW;
     const int grid = int(std::max<long long>(1, std::min<long long>(want, warps / KW)));
     a.nwarps = grid * KW;

@@ -61,6 +61,7 @@ struct InvArgs {
     int nblk_a, tb_b, split;               // ring kernel, guided tiles: blocks < nblk_a are tb rows from 0,
                                            // the rest tb_b rows from quad row `split` (nblk_a = nblk: uniform)
     long long ntiles;
+    FastDiv fd_img, fd_slabs;              // division by nblk * nslabs and by nslabs (ntiles < 2^31)
     const float *ll_lo, *ll_hi, *d_lo, *d_hi;   // allocation ranges of the LL / detail sources (ring loader)
     unsigned int *counter;                       // tile queue (queue.cuh)
     int nwarps;
@@ -223,9 +224,9 @@ __global__ void __launch_bounds__(ITHREADS, 2) dwt53_inverse_level_kernel(const 
          t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane)) {
         // tiles: image-major, then row block, then slab (adjacent slabs run together)
         const long long per_img = (long long)a.nblk * a.nslabs;
-        const int img = int(t / per_img);
+        const int img = fdiv(int(t), a.fd_img);
         const int r = int(t - (long long)img * per_img);
-        const int blk = r / a.nslabs;
+        const int blk = fdiv(r, a.fd_slabs);
         const int slab = r - blk * a.nslabs;
         const int m0 = slab * IQ;
         const int n0 = blk * a.tb, n1 = min(n0 + a.tb, Hq);
@@ -440,9 +441,9 @@ __global__ void __launch_bounds__(IRW * 32, DWT2_INV_MINB) dwt53_inverse_ring_ke
     const long long per_img = (long long)a.nblk * a.nslabs;
     for (long long t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane); t < a.ntiles;
          t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane)) {
-        const int img = int(t / per_img);
+        const int img = fdiv(int(t), a.fd_img);
         const int r = int(t - (long long)img * per_img);
-        const int blk = r / a.nslabs;
+        const int blk = fdiv(r, a.fd_slabs);
         const int slab = r - blk * a.nslabs;
         const int m0 = slab * IQ;
         const int n0 = blk < a.nblk_a ? blk * a.tb : a.split + (blk - a.nblk_a) * a.tb_b;
@@ -537,6 +538,9 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
             }
         }
         a.ntiles = (long long)a.count * a.nblk * a.nslabs;
+    a.fd_img = make_fastdiv(unsigned(a.nblk * a.nslabs));
+    a.fd_slabs = make_fastdiv(unsigned(a.nslabs));
+    if (a.ntiles >= (1LL << 31)) return fail(DWT2_EINVAL);
         const long long want = (a.ntiles + IRW - 1) / IRW;
         const int grid = int(std::max<long long>(1, std::min<long long>(want, rwarps / IRW)));
         a.nwarps = grid * IRW;
@@ -569,6 +573,9 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
     a.split = Hq;
     a.tb_b = a.tb;
     a.ntiles = (long long)a.count * a.nblk * a.nslabs;
+    a.fd_img = make_fastdiv(unsigned(a.nblk * a.nslabs));
+    a.fd_slabs = make_fastdiv(unsigned(a.nslabs));
+    if (a.ntiles >= (1LL << 31)) return fail(DWT2_EINVAL);
     const long long want = (a.ntiles + IWARPS - 1) / IWARPS;
     const int grid = int(std::max<long long>(1, std::min<long long>(want, warps / IWARPS)));
     a.nwarps = grid * IWARPS;

@@ -24,9 +24,9 @@ for W, H in zip(a[0::2], a[1::2]):
         us = time_calls(lambda q: p.inverse(q[0], q[1]), [(x, y)], 10)
     else:
         pairs = [(x, y)]
-    if os.environ.get("PROBE_COLD"):      # the bench's protocol: one buffer pair per call below 2x L2
-        pairs += [(x.clone(), torch.empty_like(y)) for _ in range(n_pairs(8 * W * H, 10) - 1)]
-    us = time_calls(lambda q: p.forward(q[0], q[1]), pairs, 10)
+        if os.environ.get("PROBE_COLD"):      # the bench's protocol (buffer pairs cycled, cold L2)
+            pairs += [(x.clone(), torch.empty_like(y)) for _ in range(n_pairs(8 * W * H, 10) - 1)]
+        us = time_calls(lambda q: p.forward(q[0], q[1]), pairs, 10)
     out.append(f"{W}x{H} {us:.1f} us ({8 * W * H / us / 1e3 / 6535:.3f})")
     p.close()
 print(" | ".join(out))
