@@ -55,7 +55,7 @@ constexpr int SLABQ = 32 * QK;             // quad columns per warp
 constexpr int OUTQ = 30 * QK;              // output quad columns per warp (lanes 1..30; lanes 0, 31: halo)
 constexpr int RW = 2 * SLABQ;              // floats per staged pixel row (= 64 QK)
 #ifndef DWT2_K2_DS
-#define DWT2_K2_DS 4                      // measured: 4 > 6 > 8 > 2 (the row loop is unrolled DS times: i-cache)
+#define DWT2_K2_DS 5                      // measured: 5 > 4 > 6 > 8 > 2 (the row loop is unrolled DS times: i-cache)
 #endif
 constexpr int DS = DWT2_K2_DS;             // raw quad rows in flight per warp (shared-memory ring, cp.async)
 constexpr int DR = 1;                      // raw quad rows in flight per warp on the register path (edge slabs)
