@@ -81,3 +81,31 @@ def test_cdf97_random(W, H, L, count, align, real, seed):
         assert np.abs(ys[i] - ref).max() <= 1e-4, f"forward 9/7 {W}x{H} L{L} image {i}"
         refi = oracle.inverse(ys[i].astype(np.float64), L, round_f32=False, wavelet="cdf97")
         assert np.abs(rec[i] - refi).max() <= 1e-4, f"inverse 9/7 {W}x{H} L{L} image {i}"
+
+
+def strip_cases(n, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        W = int(rng.integers(2, 700))
+        G = int(rng.choice([2, 3, 4, 8]))
+        L = int(rng.integers(1, 5))
+        H = int(rng.integers(2 * G * (1 << L), 2 * G * (1 << L) + 900))
+        if max_levels(W, H) < L:
+            continue
+        out.append((W, H, G, L, int(rng.integers(1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("W,H,G,L,seed", strip_cases(40, 33))
+def test_strip_pyramids_random(W, H, G, L, seed):
+    """Row strips on G emulated ranks (interior + boundary launches, one
+    ghost-row exchange per level) equal the single-GPU pyramid bit for bit."""
+    from tests.test_gpu_strip_levels import run_strip_pyramids
+    rng = np.random.default_rng(seed)
+    x = (rng.random((H, W)) * 255).astype(np.float32)
+    got = run_strip_pyramids(x, G, L, overlap=bool(seed & 1))
+    plan = dwt2.Plan(W, H, L)
+    ref = plan.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    plan.close()
+    np.testing.assert_array_equal(got, ref)
