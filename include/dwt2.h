@@ -170,6 +170,12 @@ int32_t dwt2_forward_strip_level(const dwt2_plan *plan, int32_t level, const flo
  *      read-only, 4-byte aligned.
  * out: device pointer, W x H fp32 Mallat pyramid, row pitch W, caller-owned.
  * in and out must not overlap (no in-place transform).
+ * Performance only (results are identical on every path): a 16-byte-aligned
+ * `in` is read by TMA -- 3-D tensor maps when W is a multiple of 4, row-group
+ * tensor maps (2 or 4 rows per tensor row) otherwise; an `in` that is only
+ * 4-byte aligned, or batched images with gaps between them, take a 1-D
+ * bulk-copy loader; an even ceil(W/2) with 8-byte-aligned subband rows gets
+ * vector stores.
  * Returns DWT2_OK, DWT2_EINVAL or DWT2_ECUDA. */
 int32_t dwt2_forward(const dwt2_plan *plan, const float *in, float *out, dwt2_stream_t stream);
 
