@@ -1147,7 +1147,7 @@ const TilePolicy &tile_policy()
         pol.min_tpw = env("DWT2_MIN_TPW", DWT2_MIN_TPW);
         const char *g = getenv("DWT2_GUIDED");
         pol.guided = (g && g[0] == '0') ? 0 : 1;
-        pol.guided_a = env("DWT2_GUIDED_A", 70);
+        pol.guided_a = env("DWT2_GUIDED_A", 60);   // cold-cache sweep: 55-60 > 70 > 80 on 4096^2 .. 16384 x 2048
         pol.guided_b = env("DWT2_GUIDED_B", 4);
         const char *tl = getenv("DWT2_TB_LARGE");
         pol.tb_large = tl ? atoi(tl) : 15;
@@ -1277,7 +1277,7 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     a.nblk_a = (lenA + a.tb - 1) / a.tb;
     a.nblk = a.nblk_a + (lenB + a.tb - 1) / a.tb;
     // Guided tiles for mid-size levels (few tiles per warp): one large tile
-    // per warp over ~70 % of the rows first, then the rest as ~4 small tiles
+    // per warp over ~60 % of the rows first, then the rest as ~4 small tiles
     // per warp from the queue, so warps on slower SMs (a 1.5x spread of SM
     // throughput under full HBM load) do not set the kernel's length, while
     // most rows still pay the carry-in row of a large tile only.
