@@ -525,7 +525,8 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
         static const int guided = [] { const char *v = getenv("DWT2_INV_GUIDED"); return !(v && v[0] == '0'); }();
         if (guided && a.count == 1 && slab_rows < 64 * rwarps && slab_rows >= 8 * rwarps) {
             const long long nba = std::max<long long>(1, rwarps / a.nslabs);
-            const long long tba = (7 * Hq / 10) / nba;
+            static const int pct = [] { const char *v = getenv("DWT2_INV_GUIDED_A"); return v && atoi(v) > 0 ? atoi(v) : 70; }();
+            const long long tba = (pct * Hq / 100) / nba;
             if (tba >= 16) {
                 a.tb = int(tba);
                 a.nblk_a = int(nba);
