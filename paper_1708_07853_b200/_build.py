@@ -6,13 +6,16 @@ descriptor encoder is fetched from the driver at run time).
 """
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRCS = [os.path.join(PKG, "csrc", f) for f in ("dwt2.cu", "inverse.cu", "schemes.cu", "dwt97.cu")]
-DEPS = SRCS + [os.path.join(PKG, "csrc", "dwt2_internal.h")]
+# every source and header under csrc/ (an edit to any of them rebuilds the library)
+DEPS = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")) + glob.glob(os.path.join(PKG, "csrc", "*.h")) +
+              glob.glob(os.path.join(PKG, "csrc", "*.cuh")))
 HDR = os.path.join(ROOT, "include", "dwt2.h")
 LIB = os.path.join(PKG, "libdwt2.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

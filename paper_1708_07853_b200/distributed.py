@@ -244,7 +244,9 @@ def strip_pyramid_step(pyr: StripPyramid, plan, overlap: bool = True, stream=Non
     """All levels of rank's strip: per level, the ghost-row exchange and the
     fused level kernel(s); with overlap, the interior quad rows run while the
     ghost rows are in flight, then the two boundary quad rows.  exchange(k)
-    may replace the process-group exchange (single-GPU emulation in tests).
+    may replace the process-group exchange (single-GPU emulation in tests); it
+    returns request objects whose wait() orders the current stream after the
+    ghost rows have landed, as NCCL's Work.wait() does.
 
     Measured on one B200 (scripts/strip_host_cost.py, config 3 at G = 8): the
     boundary launch right behind the interior one (programmatic dependent
@@ -277,12 +279,10 @@ def strip_pyramid_step(pyr: StripPyramid, plan, overlap: bool = True, stream=Non
         bp, bpitch, lp, lpitch = pyr._launch_args[k]
         if overlap:
             launch(h, k, bp, bpitch, lp, lpitch, out, dwt2.DWT2_STRIP_INTERIOR, sh)
-            if exchange is None:
-                pyr.finish(reqs)
+            pyr.finish(reqs)          # NCCL Work.wait(): the current stream waits for the receives
             launch(h, k, bp, bpitch, lp, lpitch, out, dwt2.DWT2_STRIP_BOUNDARY, sh)
         else:
-            if exchange is None:
-                pyr.finish(reqs)
+            pyr.finish(reqs)
             launch(h, k, bp, bpitch, lp, lpitch, out, dwt2.DWT2_STRIP_ALL, sh)
     return pyr.out
 

@@ -290,3 +290,73 @@ def test_generators_deterministic_and_ranged():
     assert not np.array_equal(s, workloads.smooth_noise(128, 96, 3))
     assert workloads.level_pixels(8192, 8192, 8) == 89_477_120
     assert workloads.CONFIGS["5"].pixels == 1_466_992_864
+
+
+# --------------------------------------------------------------------------
+# Oracle (ii): where the per-level fp32 rounding happens (DESIGN.md reading
+# C-A13: every level's whole output -- LL and the three detail bands -- is
+# stored as fp32 before the next level reads its LL).  Pinned against a
+# level-by-level composition written here: the pinned one-level oracle (i)
+# plus numpy's own fp32 rounding, applied to the region each level owns.
+# --------------------------------------------------------------------------
+def _f32(a):
+    return a.astype(np.float32).astype(np.float64)
+
+
+def _dims(W, H, L):
+    ws, hs = [W], [H]
+    for _ in range(L):
+        ws.append((ws[-1] + 1) // 2)
+        hs.append((hs[-1] + 1) // 2)
+    return ws, hs
+
+
+def _compose_forward(oracle_mod, x, L):
+    out = x.copy()
+    ws, hs = _dims(x.shape[1], x.shape[0], L)
+    for k in range(L):
+        region = np.ascontiguousarray(out[:hs[k], :ws[k]])
+        out[:hs[k], :ws[k]] = _f32(oracle_mod.forward(region, 1))
+    return out
+
+
+def _compose_inverse(oracle_mod, y, L):
+    out = y.copy()
+    ws, hs = _dims(y.shape[1], y.shape[0], L)
+    for k in range(L - 1, -1, -1):
+        region = np.ascontiguousarray(out[:hs[k], :ws[k]])
+        out[:hs[k], :ws[k]] = _f32(oracle_mod.inverse(region, 1))
+    return out
+
+
+@pytest.mark.parametrize("W,H", [(60, 50), (37, 29), (64, 64)])
+@pytest.mark.parametrize("L", [1, 2, 3])
+def test_round_f32_rounds_every_level_output(oracle_mod, W, H, L):
+    x = np.random.default_rng(W * 7 + H + L).uniform(0, 255, (H, W)).astype(np.float32).astype(np.float64)
+    y = oracle_mod.forward(x, L, round_f32=True)
+    # every stored coefficient (every level, every subband) is an fp32 value
+    np.testing.assert_array_equal(y, _f32(y))
+    # and equals the level-by-level composition with fp32 storage between levels
+    np.testing.assert_array_equal(y, _compose_forward(oracle_mod, x, L))
+    if L == 1:
+        np.testing.assert_array_equal(y, _f32(oracle_mod.forward(x, 1)))
+    # the composition is discriminating: rounding only at the end differs
+    if L >= 2:
+        assert not np.array_equal(y, _f32(oracle_mod.forward(x, L)))
+
+
+@pytest.mark.parametrize("W,H", [(60, 50), (37, 29)])
+@pytest.mark.parametrize("L", [1, 2, 3])
+def test_inverse_round_f32_rounds_every_level(oracle_mod, W, H, L):
+    rng = np.random.default_rng(W + H * 3 + L)
+    # a real-valued fp32 pyramid (not the transform of anything in particular)
+    y = rng.uniform(-300, 300, (H, W)).astype(np.float32).astype(np.float64)
+    r = oracle_mod.inverse(y, L, round_f32=True)
+    np.testing.assert_array_equal(r, _f32(r))
+    np.testing.assert_array_equal(r, _compose_inverse(oracle_mod, y, L))
+    if L >= 2:
+        assert not np.array_equal(r, _f32(oracle_mod.inverse(y, L)))
+    # fp64 inverse with per-level rounding still reconstructs a real image to fp32 accuracy
+    x = rng.uniform(0, 255, (H, W)).astype(np.float32).astype(np.float64)
+    rt = oracle_mod.inverse(oracle_mod.forward(x, L, round_f32=True), L, round_f32=True)
+    assert np.abs(rt - x).max() < 1e-4
