@@ -1120,8 +1120,8 @@ struct LaunchIO {
 };
 
 // Tile-size policy of the work queue (measured on B200).
-// DWT2_TPW / DWT2_MIN_TB / DWT2_MIN_TPW in the environment override it for
-// tuning sweeps (read once per process).
+// A -DDWT2_TUNING build reads DWT2_TPW, DWT2_MIN_TB, ... from the environment
+// for sweeps (tuning_int, read once per process); the product build does not.
 struct TilePolicy {
     int tpw;       // target tiles per warp on large levels
     int min_tb;    // minimum quad rows per tile
@@ -1138,20 +1138,14 @@ const TilePolicy &tile_policy()
     static TilePolicy pol;
     static std::once_flag once;
     std::call_once(once, [] {
-        auto env = [](const char *name, int dflt) {
-            const char *v = getenv(name);
-            return (v && atoi(v) > 0) ? atoi(v) : dflt;
-        };
-        pol.tpw = env("DWT2_TPW", DWT2_TPW);
-        pol.min_tb = env("DWT2_MIN_TB", MIN_TILE_ROWS);
-        pol.min_tpw = env("DWT2_MIN_TPW", DWT2_MIN_TPW);
-        const char *g = getenv("DWT2_GUIDED");
-        pol.guided = (g && g[0] == '0') ? 0 : 1;
-        pol.guided_a = env("DWT2_GUIDED_A", 60);   // cold-cache sweep: 55-60 > 70 > 80 on 4096^2 .. 16384 x 2048
-        pol.guided_b = env("DWT2_GUIDED_B", 4);
-        const char *tl = getenv("DWT2_TB_LARGE");
-        pol.tb_large = tl ? atoi(tl) : 15;
-        pol.large_tpw = env("DWT2_LARGE_TPW", 9);
+        pol.tpw = tuning_int("DWT2_TPW", DWT2_TPW, 1, 1024);
+        pol.min_tb = tuning_int("DWT2_MIN_TB", MIN_TILE_ROWS, PAIRS - 1, MAX_TILE_ROWS);
+        pol.min_tpw = tuning_int("DWT2_MIN_TPW", DWT2_MIN_TPW, 1, 1024);
+        pol.guided = tuning_int("DWT2_GUIDED", 1, 0, 1);
+        pol.guided_a = tuning_int("DWT2_GUIDED_A", 60, 10, 90);   // cold-cache sweep: 55-60 > 70 > 80 on 4096^2 .. 16384 x 2048
+        pol.guided_b = tuning_int("DWT2_GUIDED_B", 4, 1, 64);
+        pol.tb_large = tuning_int("DWT2_TB_LARGE", 15, 0, MAX_TILE_ROWS);
+        pol.large_tpw = tuning_int("DWT2_LARGE_TPW", 9, 1, 1024);
     });
     return pol;
 }
@@ -1286,10 +1280,10 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
         const long long nblk_a = std::max<long long>(1, warps_full / a.nslabs);
         long long tb_a = (pol.guided_a * lenA / 100) / nblk_a;
         tb_a = (tb_a + 1) / PAIRS * PAIRS - 1;                       // tb + 1 whole stages, rounded down
-        if (tb_a >= 2 * PAIRS - 1) {
-            const long long rows_a = nblk_a * tb_a, rest = lenA - rows_a;
+        if (tb_a >= 2 * PAIRS - 1 && nblk_a * tb_a < lenA) {
+            const long long rows_a = nblk_a * tb_a, rest = lenA - rows_a;     // rest > 0
             long long tb_b = rest * a.nslabs / ((long long)pol.guided_b * warps_full);
-            static const int min_b = [] { const char *v = getenv("DWT2_GUIDED_MINB"); return v && atoi(v) > 0 ? atoi(v) : 2; }();
+            static const int min_b = tuning_int("DWT2_GUIDED_MINB", 2, 1, 16);
             tb_b = std::max<long long>(min_b * PAIRS - 1, (tb_b + 1 + PAIRS - 1) / PAIRS * PAIRS - 1);
             a.tb = int(tb_a);
             a.tb_b = int(std::min<long long>(tb_b, MAX_TILE_ROWS));
@@ -1314,8 +1308,8 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     // row-grouped loader (4096^2 0.79 -> 0.85, 16384 x 2048 0.85 -> 0.87,
     // 2048^2 0.55 -> 0.60, 8193^2 0.85 -> 0.87, 4095 x 3001 0.60 -> 0.68) but
     // slower on large 3-D TMA levels (8192^2 0.94 -> 0.83, 16384^2 0.98 ->
-    // 0.97), for reasons not established; DWT2_UNROLL_FIRST=0/1 forces it
-    static const int env_uf = [] { const char *v = getenv("DWT2_UNROLL_FIRST"); return v ? atoi(v) : -1; }();
+    // 0.97), for reasons not established; DWT2_UNROLL_FIRST=0/1 forces it (tuning builds)
+    static const int env_uf = tuning_int("DWT2_UNROLL_FIRST", -1, 0, 1);
     a.unroll_first = env_uf >= 0 ? env_uf : ((a.tb_b != a.tb || a.qb1 > a.qb0 || grp || a.static_tiles) ? 1 : 0);
     a.counter = p->counters + 2 * ((queue ? QUEUE_STRIP_BOUNDARY : QUEUE_FORWARD) + level);
 
@@ -1490,21 +1484,16 @@ namespace dwt2_detail {
 
 thread_local int32_t g_last_error = DWT2_OK;
 
+// Checked on every call (no cache: a freed and re-used address must not pass
+// on the strength of an earlier check).
 bool on_plan_device(const dwt2_plan *p, const void *ptr)
 {
-    for (int i = 0; i < 4; ++i)
-        if (p->valid_ptr[i] == ptr) return true;
     cudaPointerAttributes at;
     if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
-    const bool ok = (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) && at.device == p->device;
-    if (ok) {
-        p->valid_ptr[p->valid_next] = ptr;
-        p->valid_next = (p->valid_next + 1) & 3;
-    }
-    return ok;
+    return (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) && at.device == p->device;
 }
 
 }  // namespace dwt2_detail
@@ -1801,6 +1790,47 @@ int32_t dwt2_forward_strip(const dwt2_plan *p, const float *in, float *out, int3
     return dwt2_forward_strip_level(p, 0, in, p->W, nullptr, 0, out, part, stream);
 }
 
+}  // extern "C"
+
+namespace {
+
+// Releases whatever host_staging_create acquired (any subset) and marks the
+// plan as having no staging (d_in == nullptr).
+void host_staging_release(const dwt2_plan *p)
+{
+    if (p->d_in) cudaFree(p->d_in);
+    if (p->d_out) cudaFree(p->d_out);
+    if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
+    if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
+    for (int i = 0; i < 132; ++i)
+        if (p->ev[i]) cudaEventDestroy(p->ev[i]);
+    p->d_in = p->d_out = nullptr;
+    p->s_h2d = p->s_d2h = nullptr;
+    for (int i = 0; i < 132; ++i) p->ev[i] = nullptr;
+    cudaGetLastError();
+}
+
+// All-or-nothing: device staging buffers, the copy streams and the events of
+// dwt2_forward_host.  On failure nothing stays allocated and d_in stays null.
+int32_t host_staging_create(const dwt2_plan *p, long long npx)
+{
+    int32_t code = DWT2_OK;
+    if (cudaMalloc(&p->d_in, npx * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&p->d_out, npx * sizeof(float)) != cudaSuccess)
+        code = DWT2_ENOMEM;
+    else if (cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+             cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking) != cudaSuccess)
+        code = DWT2_ECUDA;
+    for (int i = 0; code == DWT2_OK && i < 132; ++i)
+        if (cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming) != cudaSuccess) code = DWT2_ECUDA;
+    if (code != DWT2_OK) host_staging_release(p);
+    return code;
+}
+
+}  // namespace
+
+extern "C" {
+
 int32_t dwt2_forward_host(const dwt2_plan *p, const float *host_in, float *host_out, dwt2_stream_t stream)
 {
     if (!p || !host_in || !host_out || p->strip || p->max_count != 1) return fail(DWT2_EINVAL);
@@ -1808,27 +1838,13 @@ int32_t dwt2_forward_host(const dwt2_plan *p, const float *host_in, float *host_
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const long long npx = (long long)p->W * p->H;
     if (!p->d_in) {
-        if (cudaMalloc(&p->d_in, npx * sizeof(float)) != cudaSuccess ||
-            cudaMalloc(&p->d_out, npx * sizeof(float)) != cudaSuccess) {
-            cudaGetLastError();
-            if (p->d_in) cudaFree(p->d_in);
-            p->d_in = p->d_out = nullptr;
-            return fail(DWT2_ENOMEM);
-        }
-        if (cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking) != cudaSuccess)
-            return fail(DWT2_ECUDA);
-        for (int i = 0; i < 132; ++i)
-            if (cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming) != cudaSuccess) return fail(DWT2_ECUDA);
+        int32_t st = host_staging_create(p, npx);
+        if (st != DWT2_OK) return fail(st);
     }
     // Pipeline over NB row bands of level 1: H2D(band b) -> kernel on the
     // quad rows whose inputs have all arrived -> D2H of finished output rows.
     const LevelGeom &g = p->geom[0];
-    static const int max_bands = [] {
-        const char *v = getenv("DWT2_HOST_BANDS");        // tuning override
-        const int n = v ? atoi(v) : 0;
-        return (n >= 1 && n <= 64) ? n : 16;   // 16 = 32 = 11.5 Gpix/s at config 3 (PCIe-bound)
-    }();
+    static const int max_bands = tuning_int("DWT2_HOST_BANDS", 16, 1, 64);   // 16 = 32: 11.5 Gpix/s at config 3 (PCIe-bound)
     const int NB = std::min(max_bands, std::max(1, g.Hq / 64));
     const size_t rowb = size_t(p->W) * sizeof(float);
     cudaEvent_t *ev_in = p->ev, *ev_k = p->ev + 64, *ev_done = p->ev + 128;
@@ -1895,13 +1911,7 @@ void dwt2_destroy(dwt2_plan *p)
     for (int s = 0; s < 2; ++s)
         if (p->scratch[s]) cudaFree(p->scratch[s]);
     if (p->work) cudaFree(p->work);
-    if (p->d_in) {
-        cudaFree(p->d_in);
-        cudaFree(p->d_out);
-        cudaStreamDestroy(p->s_h2d);
-        cudaStreamDestroy(p->s_d2h);
-        for (int i = 0; i < 132; ++i) cudaEventDestroy(p->ev[i]);
-    }
+    host_staging_release(p);
     cudaGetLastError();
     delete p;
 }

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/dwt2.h"
 
@@ -45,6 +46,22 @@ inline FastDiv make_fastdiv(unsigned d)
 __device__ __forceinline__ int fdiv(int n, FastDiv f)
 {
     return int((__umulhi(unsigned(n), f.mul) + unsigned(n)) >> f.shift);
+}
+
+// Tile-policy knobs for measurement sweeps.  Only a -DDWT2_TUNING build
+// (build/variants, _build.build_variant) reads them from the environment, and
+// only inside [lo, hi]; the product library always uses the measured defaults,
+// so its performance does not depend on the caller's environment.
+inline int tuning_int(const char *name, int dflt, int lo, int hi)
+{
+#ifdef DWT2_TUNING
+    if (const char *v = getenv(name)) {
+        const int x = atoi(v);
+        if (x >= lo && x <= hi) return x;
+    }
+#endif
+    (void)name; (void)lo; (void)hi;
+    return dflt;
 }
 
 struct LevelGeom {
@@ -100,8 +117,6 @@ struct dwt2_plan {
         CUtensorMap map, map_b;
     };
     mutable TmapCache tcache[dwt2_detail::MAX_LEVELS];
-    mutable const void *valid_ptr[4];       // device pointers already checked by on_plan_device
-    mutable int valid_next;
     // scheme variants (schemes.cu): one full-size work buffer, allocated lazily
     mutable float *work;
     mutable size_t work_bytes;
@@ -113,7 +128,7 @@ struct dwt2_plan {
 
 namespace dwt2_detail {
 
-// true if ptr is device (or managed) memory of the plan's device (cached)
+// true if ptr is device (or managed) memory of the plan's device
 bool on_plan_device(const dwt2_plan *p, const void *ptr);
 
 // forward of `count` images with the literal (variant 1) or adapted (2)

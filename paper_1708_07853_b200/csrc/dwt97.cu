@@ -429,9 +429,9 @@ int32_t launch_k2_level(const dwt2_plan *p, K2Args a, cudaStream_t s)
     // (measured: 0.62 -> 0.77 of copy at 16384^2 from 4 to 16 tiles per warp,
     // 0.80 -> 0.86 from 16 to 32; the 4 warm-up rows per tile cost less than
     // the imbalance), scripts/sweeps/gpu_queue_tpw.sh, scripts/tile_probe.py
-    static const int tpw = [] { const char *v = getenv("DWT2_K2_TPW"); return v && atoi(v) > 0 ? atoi(v) : 32; }();
+    static const int tpw = tuning_int("DWT2_K2_TPW", 32, 1, 1024);
     long long tb = slab_rows / (tpw * warps);
-    static const int min_tb = [] { const char *v = getenv("DWT2_K2_MINTB"); return v && atoi(v) > 0 ? atoi(v) : 16; }();
+    static const int min_tb = tuning_int("DWT2_K2_MINTB", 16, 4, 512);
     tb = std::max<long long>(min_tb, std::min<long long>(512, tb)); // 4 warm-up rows per tile: >= 16 rows
     a.tb = int(tb);
     a.nblk = int((Hq + tb - 1) / tb);
@@ -756,14 +756,14 @@ int32_t launch_k2_inverse_level(const dwt2_plan *p, K2InvArgs a, cudaStream_t s)
     a.nslabs = (Wq + OUTQ - 1) / OUTQ;
     const long long warps = (long long)p->sms * per_sm * KW;
     const long long slab_rows = (long long)a.count * a.nslabs * Hq;
-    static const int tpw = [] { const char *v = getenv("DWT2_K2INV_TPW"); return v && atoi(v) > 0 ? atoi(v) : 8; }();
+    static const int tpw = tuning_int("DWT2_K2INV_TPW", 8, 1, 1024);
     long long tb = slab_rows / (tpw * warps);
-    static const int min_tb = [] { const char *v = getenv("DWT2_K2INV_MINTB"); return v && atoi(v) > 0 ? atoi(v) : 16; }();
+    static const int min_tb = tuning_int("DWT2_K2INV_MINTB", 16, 4, 512);
     tb = std::max<long long>(min_tb, std::min<long long>(512, tb));
     // levels with >= 64 quad rows per warp: 20-row tiles (measured: 16384^2
     // 0.765 -> 0.766, 16384 x 6144 0.64 -> 0.70, 8192^2 0.638 -> 0.644 of copy
     // against the tpw-derived height; smaller levels keep it)
-    static const int tb_large = [] { const char *v = getenv("DWT2_K2INV_TB"); return v ? atoi(v) : 20; }();
+    static const int tb_large = tuning_int("DWT2_K2INV_TB", 20, 0, 512);
     if (tb_large > 0 && slab_rows >= 64 * warps) tb = tb_large;
     a.tb = int(tb);
     a.nblk = int((Hq + tb - 1) / tb);

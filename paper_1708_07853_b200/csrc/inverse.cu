@@ -504,7 +504,7 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
         // tiles per warp for the queue: 16 on large levels (balance), 4 on
         // mid-size ones (the seed row of a tile costs more there); measured,
         // scripts/sweeps/gpu_queue_tpw.sh
-        static const int env_tpw = [] { const char *v = getenv("DWT2_INV_TPW"); return v ? atoi(v) : 0; }();
+        static const int env_tpw = tuning_int("DWT2_INV_TPW", 0, 1, 1024);
         const int tpw = env_tpw > 0 ? env_tpw : (slab_rows >= 256 * rwarps ? 16 : 4);
         long long tb = slab_rows / (tpw * rwarps);
         tb = std::max<long long>(8, std::min<long long>(256, tb));
@@ -512,7 +512,7 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
         // 8192^2 .. 16384^2 against 8, 12, 16, 24, 27..55-row tiles and the
         // guided split: 16384 x 8192 0.80 -> 0.88, 16384^2 0.89 -> 0.91,
         // 8192^2 0.81 -> 0.83 of copy); guided tiles below 64 rows per warp
-        static const int env_tb = [] { const char *v = getenv("DWT2_INV_TB"); return v ? atoi(v) : 20; }();
+        static const int env_tb = tuning_int("DWT2_INV_TB", 20, 0, 256);
         if (env_tpw <= 0 && env_tb > 0 && slab_rows >= 64 * rwarps) tb = env_tb;
         a.tb = int(tb);
         a.nblk = int((Hq + tb - 1) / tb);
@@ -522,10 +522,10 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
         // guided tiles on mid-size levels (few tiles per warp): one large tile
         // per warp over ~70 % of the rows, then ~4 small tiles per warp (as
         // the forward kernel, dwt2.cu)
-        static const int guided = [] { const char *v = getenv("DWT2_INV_GUIDED"); return !(v && v[0] == '0'); }();
+        static const int guided = tuning_int("DWT2_INV_GUIDED", 1, 0, 1);
         if (guided && a.count == 1 && slab_rows < 64 * rwarps && slab_rows >= 8 * rwarps) {
             const long long nba = std::max<long long>(1, rwarps / a.nslabs);
-            static const int pct = [] { const char *v = getenv("DWT2_INV_GUIDED_A"); return v && atoi(v) > 0 ? atoi(v) : 70; }();
+            static const int pct = tuning_int("DWT2_INV_GUIDED_A", 70, 10, 90);
             const long long tba = (pct * Hq / 100) / nba;
             if (tba >= 16) {
                 a.tb = int(tba);
@@ -565,7 +565,7 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
     // tile height: ~8 tiles per resident warp, at least 8 quad rows (the
     // halo row re-read costs 1 / tb), at most 256
     long long slab_rows = (long long)a.count * a.nslabs * Hq;
-    static const int ldg_tpw = [] { const char *v = getenv("DWT2_INV_LDG_TPW"); return v && atoi(v) > 0 ? atoi(v) : 8; }();
+    static const int ldg_tpw = tuning_int("DWT2_INV_LDG_TPW", 8, 1, 1024);
     long long tb = slab_rows / (ldg_tpw * warps);
     tb = std::max<long long>(8, std::min<long long>(256, tb));
     a.tb = int(tb);

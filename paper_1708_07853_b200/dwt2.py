@@ -13,7 +13,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("DWT2_LIB") or os.path.join(_PKG, "libdwt2.so")   # DWT2_LIB: tuning variants
+LIB_PATH = os.path.join(_PKG, "libdwt2.so")      # the in-tree product library (no environment override)
 
 DWT2_OK, DWT2_EINVAL, DWT2_ENOMEM, DWT2_ECUDA, DWT2_EUNSUPPORTED = 0, -1, -2, -3, -4
 DWT2_BOUNDARY_SYMMETRIC = 0
@@ -71,6 +71,16 @@ class DWT2Error(RuntimeError):
     def __init__(self, code: int, what: str):
         self.code = code
         super().__init__(f"{what}: {error_string(code)} ({code})")
+
+
+def use_variant(path: str) -> None:
+    """Measurement scripts only: load a tuning build (build/variants/, see
+    _build.build_variant) instead of the product library.  Must be called
+    before the first call into the library."""
+    global LIB_PATH
+    if _lib is not None:
+        raise RuntimeError("libdwt2 is already loaded")
+    LIB_PATH = os.path.abspath(path)
 
 
 def lib() -> ctypes.CDLL:
@@ -292,7 +302,17 @@ class Plan:
         return out
 
     def forward_host(self, host_in, host_out, stream=None):
-        """host_in / host_out: CPU float32 tensors (pinned for full speed)."""
+        """host_in / host_out: CPU float32 contiguous H x W tensors (pinned for
+        full speed).  Checked here because the C call copies W*H floats from
+        and to the raw host pointers."""
+        import torch
+        for name, t in (("host_in", host_in), ("host_out", host_out)):
+            if not isinstance(t, torch.Tensor) or t.device.type != "cpu" or t.dtype != torch.float32 \
+                    or not t.is_contiguous() or t.numel() != self.width * self.height:
+                raise ValueError(f"{name}: need a contiguous CPU float32 tensor of {self.height} x {self.width} "
+                                 f"elements")
+        if self.max_count != 1:
+            raise ValueError("forward_host: single-image plans only")
         dwt2_forward_host(self._p, host_in.data_ptr(), host_out.data_ptr(), _stream_handle(stream))
         return host_out
 

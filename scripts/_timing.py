@@ -7,6 +7,8 @@ tick every 2.048 us on this driver (scripts/diag_small.py), so single short
 calls are never bracketed alone."""
 import torch
 
+import _variant  # noqa: F401  (DWT2_LIB: tuning / profiling builds)
+
 L2_BYTES = 126e6
 _flush = None
 

@@ -13,6 +13,8 @@ import torch
 sys.path.insert(0, ".")
 sys.path.insert(0, "scripts")
 from _timing import time_calls  # noqa: E402
+sys.path.insert(0, "scripts")
+import _variant  # noqa: E402,F401
 from paper_1708_07853_b200 import dwt2, workloads  # noqa: E402
 
 torch.cuda.set_device(0)

@@ -2,6 +2,8 @@
 import ctypes, sys
 import numpy as np, torch
 sys.path.insert(0, '.')
+sys.path.insert(0, "scripts")
+import _variant  # noqa: E402,F401
 from paper_1708_07853_b200 import dwt2, workloads
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 H = int(sys.argv[2]) if len(sys.argv) > 2 else W
