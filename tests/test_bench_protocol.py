@@ -40,3 +40,68 @@ def test_small_configs_flagged():
     assert bench.buffer_pairs(workloads.CONFIGS["1"], 20) == 20
     assert bench.buffer_pairs(workloads.CONFIGS["2"], 20) == 3
     assert bench.buffer_pairs(workloads.CONFIGS["3"], 20) == 1
+
+
+# --------------------------------------------------------------------------
+# the correctness gate's host logic (bench.gate), on CPU tensors: a stand-in
+# runner whose "timed output" is the oracle's own pyramid must pass, and the
+# same output with one coefficient moved by one fp32 ulp must fail -- in the
+# whole-output mode and in the sampled (border quads + random positions) mode
+# --------------------------------------------------------------------------
+import types  # noqa: E402
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+
+def _fake_single_runner(cfg, out_np, img):
+    r = types.SimpleNamespace()
+    r.torch = torch
+    r.mode = "single"
+    r.nbuf = 2
+    r.i = 1
+    r.outs = [torch.from_numpy(out_np.copy()), torch.from_numpy(out_np.copy())]
+    r.host_img = img
+    r.x = torch.from_numpy(img)
+    return r
+
+
+def _args(**kw):
+    d = dict(wavelet="cdf53", op="forward", scheme="fused")
+    d.update(kw)
+    return types.SimpleNamespace(**d)
+
+
+@pytest.mark.parametrize("full", [True, False])
+def test_gate_passes_oracle_output_and_flags_one_ulp(oracle_mod, monkeypatch, full):
+    cfg = workloads.Config("t", 1, (workloads.ImageGroup(300, 212, 1, "uniform", 9),), "test")
+    img = cfg.groups[0].image(0)
+    ref = oracle_mod.forward(img.astype(np.float64), 1, round_f32=True).astype(np.float32)
+    if not full:
+        monkeypatch.setattr(bench, "GATE_FULL_PX", 0)
+    res = bench.gate(_fake_single_runner(cfg, ref, img), cfg, _args())
+    assert res["status"] == "pass", res
+    assert res["elements_checked"] >= (300 * 212 if full else 4 * bench.GATE_RANDOM)
+    # a border coefficient (HH at quad (0, last row)) one ulp off
+    bad = ref.copy()
+    r, c = 211 // 2 + 105, 150 + 0
+    bad[r, c] = np.nextafter(bad[r, c], np.float32(np.inf))
+    res = bench.gate(_fake_single_runner(cfg, bad, img), cfg, _args())
+    assert res["status"] == "fail" and "bit-exact" in res["error"], res
+
+
+def test_gate_positions_cover_every_border_and_strip_edges():
+    rng = np.random.default_rng(0)
+    W, H = 101, 64
+    b, m, n = bench._positions(W, H, [0, 1, 2, 3], rng)
+    for band, (_, _, rows, cols) in enumerate(bench._bands1(W, H)):
+        sel = b == band
+        for col in (0, 1, cols - 2, cols - 1):
+            assert set(range(rows)) <= set(n[sel & (m == col)])
+        for row in (0, 1, rows - 2, rows - 1):
+            assert set(range(cols)) <= set(m[sel & (n == row)])
+    # a strip's quad rows [10, 20): only those rows, including its own first / last two
+    b, m, n = bench._positions(W, H, [1, 3], rng, 10, 20)
+    assert n.min() >= 10 and n.max() < 20
+    for row in (10, 11, 18, 19):
+        assert set(range(W // 2)) <= set(m[(b == 3) & (n == row)])
