@@ -21,7 +21,8 @@ constexpr int MAX_LEVELS = 32;
 constexpr int QUEUE_FORWARD = 0;                  // forward level kernels (5/3 or K = 2)
 constexpr int QUEUE_STRIP_BOUNDARY = MAX_LEVELS;  // strip BOUNDARY launches (may overlap INTERIOR)
 constexpr int QUEUE_INVERSE = 2 * MAX_LEVELS;     // inverse level kernels
-constexpr int QUEUE_SLOTS = 3 * MAX_LEVELS;
+constexpr int QUEUE_TAIL = 3 * MAX_LEVELS;        // tail kernel: [0] grid-barrier arrivals, [1] CTAs done
+constexpr int QUEUE_SLOTS = 3 * MAX_LEVELS + 1;
 
 // Division by a launch-constant divisor without the integer-divide sequence
 // (decode_tile runs twice per tile; ncu had its two divisions at 3.5 % of the
