@@ -134,16 +134,24 @@ __device__ __forceinline__ RawRow load_raw_row(const K2Args &a, const float *img
     return R;
 }
 
+// Register arithmetic type: fp64 (the product); -DDWT2_K2_F32 builds an fp32
+// variant that exists to measure what the fp64 arithmetic costs.
+#ifdef DWT2_K2_F32
+typedef float k2r;
+#else
+typedef double k2r;
+#endif
+
 // carried state per quad (see the step comments in the kernel)
 struct Carry2 {
-    double a, c, d, hl1;        // raw a, c, d and predict-1 HL' of row r-1
-    double hh1, lh1f;           // predict-1 HH' and update-1 LH of row r-2
-    double A, hl2;              // update-1 LL and predict-2 HL' of row r-2
-    double hh2, lh2f;           // predict-2 HH' and update-2 LH of row r-3
+    k2r a, c, d, hl1;        // raw a, c, d and predict-1 HL' of row r-1
+    k2r hh1, lh1f;           // predict-1 HH' and update-1 LH of row r-2
+    k2r A, hl2;              // update-1 LL and predict-2 HL' of row r-2
+    k2r hh2, lh2f;           // predict-2 HH' and update-2 LH of row r-3
 };
 
-__device__ __forceinline__ double shr(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }   // lane + 1
-__device__ __forceinline__ double shl(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }     // lane - 1
+__device__ __forceinline__ k2r shr(k2r v) { return __shfl_down_sync(0xffffffffu, v, 1); }   // lane + 1
+__device__ __forceinline__ k2r shl(k2r v) { return __shfl_up_sync(0xffffffffu, v, 1); }     // lane - 1
 
 // horizontal neighbours of quad i of the lane: i + 1 (lane + 1's quad 0 for
 // the last) and i - 1 (lane - 1's last quad for the first)
@@ -218,74 +226,74 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
             R = reg[ASYNC ? 0 : j];
         }
         if (!ASYNC) issue(j, r + D);
-        double av[QK], bv[QK], cv[QK], dv[QK];
+        k2r av[QK], bv[QK], cv[QK], dv[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) {
             av[i] = R.e[2 * i]; bv[i] = R.e[2 * i + 1];
             cv[i] = R.o[2 * i]; dv[i] = R.o[2 * i + 1];
         }
         // ---- predict 1, row r (same-row part): HL'1 = b + c0 (a + a[m+1])
-        const double a_nb = shr(av[0]);
-        double hl1[QK];
+        const k2r a_nb = shr(av[0]);
+        k2r hl1[QK];
 #pragma unroll
-        for (int i = 0; i < QK; ++i) hl1[i] = fma(a.c0, av[i] + K2_RIGHT(av, i, a_nb), bv[i]);
+        for (int i = 0; i < QK; ++i) hl1[i] = fma(k2r(a.c0), av[i] + K2_RIGHT(av, i, a_nb), bv[i]);
         // ---- predict 1 completes row r-1: LH'1 = c + c0 (a + a[n+1]),
         //      HH'1 = d + c0 (c + c[m+1]) + c0 (HL'1 + HL'1[n+1])
-        double cp_[QK];
+        k2r cp_[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) cp_[i] = cy[i].c;
-        const double c_nb = shr(cp_[0]);
-        double lh1[QK], hh1[QK];
+        const k2r c_nb = shr(cp_[0]);
+        k2r lh1[QK], hh1[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) {
-            lh1[i] = fma(a.c0, cy[i].a + av[i], cy[i].c);
-            hh1[i] = fma(a.c0, cy[i].hl1 + hl1[i], fma(a.c0, cy[i].c + K2_RIGHT(cp_, i, c_nb), cy[i].d));
+            lh1[i] = fma(k2r(a.c0), cy[i].a + av[i], cy[i].c);
+            hh1[i] = fma(k2r(a.c0), cy[i].hl1 + hl1[i], fma(k2r(a.c0), cy[i].c + K2_RIGHT(cp_, i, c_nb), cy[i].d));
         }
         // ---- update 1, row r-1: LH1 = LH'1 + c1 (HH'1 + HH'1[m-1]),
         //      HL1 = HL'1 + c1 (HH'1 + HH'1[n-1]),
         //      LL1 = a + c1 (HL'1 + HL'1[m-1]) + c1 (LH1 + LH1[n-1])
-        double hlp[QK];
+        k2r hlp[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) hlp[i] = cy[i].hl1;
-        const double hh1_l = shl(hh1[QK - 1]);
-        const double hl1p_l = shl(hlp[QK - 1]);
-        double A1[QK], B1[QK], C1[QK];
+        const k2r hh1_l = shl(hh1[QK - 1]);
+        const k2r hl1p_l = shl(hlp[QK - 1]);
+        k2r A1[QK], B1[QK], C1[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) {
-            C1[i] = fma(a.c1, hh1[i] + K2_LEFT(hh1, i, hh1_l), lh1[i]);
-            B1[i] = fma(a.c1, hh1[i] + cy[i].hh1, cy[i].hl1);
-            A1[i] = fma(a.c1, C1[i] + cy[i].lh1f, fma(a.c1, cy[i].hl1 + K2_LEFT(hlp, i, hl1p_l), cy[i].a));
+            C1[i] = fma(k2r(a.c1), hh1[i] + K2_LEFT(hh1, i, hh1_l), lh1[i]);
+            B1[i] = fma(k2r(a.c1), hh1[i] + cy[i].hh1, cy[i].hl1);
+            A1[i] = fma(k2r(a.c1), C1[i] + cy[i].lh1f, fma(k2r(a.c1), cy[i].hl1 + K2_LEFT(hlp, i, hl1p_l), cy[i].a));
         }
         // ---- predict 2 on the update-1 output, row r-1 (same-row part):
         //      HL'2 = HL1 + c2 (LL1 + LL1[m+1])
-        const double A_nb = shr(A1[0]);
-        double hl2[QK];
+        const k2r A_nb = shr(A1[0]);
+        k2r hl2[QK];
 #pragma unroll
-        for (int i = 0; i < QK; ++i) hl2[i] = fma(a.c2, A1[i] + K2_RIGHT(A1, i, A_nb), B1[i]);
+        for (int i = 0; i < QK; ++i) hl2[i] = fma(k2r(a.c2), A1[i] + K2_RIGHT(A1, i, A_nb), B1[i]);
         // ---- predict 2 completes row r-2 (carried A, LH1 = lh1f, HH1 = hh1, HL'2):
         //      LH'2 = LH1 + c2 (LL1 + LL1[n+1]), HH'2 = HH1 + c2 (LH1 + LH1[m+1]) + c2 (HL'2 + HL'2[n+1])
-        double lf[QK];
+        k2r lf[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) lf[i] = cy[i].lh1f;
-        const double C_nb = shr(lf[0]);
-        double lh2[QK], hh2[QK];
+        const k2r C_nb = shr(lf[0]);
+        k2r lh2[QK], hh2[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) {
-            lh2[i] = fma(a.c2, cy[i].A + A1[i], cy[i].lh1f);
-            hh2[i] = fma(a.c2, cy[i].hl2 + hl2[i], fma(a.c2, cy[i].lh1f + K2_RIGHT(lf, i, C_nb), cy[i].hh1));
+            lh2[i] = fma(k2r(a.c2), cy[i].A + A1[i], cy[i].lh1f);
+            hh2[i] = fma(k2r(a.c2), cy[i].hl2 + hl2[i], fma(k2r(a.c2), cy[i].lh1f + K2_RIGHT(lf, i, C_nb), cy[i].hh1));
         }
         // ---- update 2, row r-2
-        double h2p[QK];
+        k2r h2p[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) h2p[i] = cy[i].hl2;
-        const double hh2_l = shl(hh2[QK - 1]);
-        const double hl2p_l = shl(h2p[QK - 1]);
-        double A2[QK], B2[QK], C2[QK];
+        const k2r hh2_l = shl(hh2[QK - 1]);
+        const k2r hl2p_l = shl(h2p[QK - 1]);
+        k2r A2[QK], B2[QK], C2[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) {
-            C2[i] = fma(a.c3, hh2[i] + K2_LEFT(hh2, i, hh2_l), lh2[i]);
-            B2[i] = fma(a.c3, hh2[i] + cy[i].hh2, cy[i].hl2);
-            A2[i] = fma(a.c3, C2[i] + cy[i].lh2f, fma(a.c3, cy[i].hl2 + K2_LEFT(h2p, i, hl2p_l), cy[i].A));
+            C2[i] = fma(k2r(a.c3), hh2[i] + K2_LEFT(hh2, i, hh2_l), lh2[i]);
+            B2[i] = fma(k2r(a.c3), hh2[i] + cy[i].hh2, cy[i].hl2);
+            A2[i] = fma(k2r(a.c3), C2[i] + cy[i].lh2f, fma(k2r(a.c3), cy[i].hl2 + K2_LEFT(h2p, i, hl2p_l), cy[i].A));
         }
         // ---- store output row r-2 (scaled)
         const int n = r - 2;
@@ -502,8 +510,8 @@ struct K2InvArgs {
 };
 
 struct InvCarry {
-    double hh2, lh, hl2p, lh2p, ll1;        // row n-1: scaled HH, input LH, HL'2, LH'2, LL1
-    double hh1, lh1, a, hl1p, lh1p;         // row n-2: HH1, LH1, a, HL'1, LH'1
+    k2r hh2, lh, hl2p, lh2p, ll1;        // row n-1: scaled HH, input LH, HL'2, LH'2, LL1
+    k2r hh1, lh1, a, hl1p, lh1p;         // row n-2: HH1, LH1, a, HL'1, LH'1
 };
 
 __device__ __forceinline__ int mqi(int q, int par, int n) { return (wssi(2 * q + par, n) - par) >> 1; }
@@ -596,75 +604,75 @@ __device__ void kinv_tile(const K2InvArgs &a, float *ring, int img, int m0, int 
             R = reg[ASYNC ? 0 : j];
             issue(j, n + D);
         }
-        double LL[2], HL[2], LH[2], HH[2];
+        k2r LL[2], HL[2], LH[2], HH[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             LL[i] = R.LL[i]; HL[i] = R.HL[i]; LH[i] = R.LH[i]; HH[i] = R.HH[i];
         }
         // ---- scaling undone, undo U2 at row n
-        double a2[2], hh2[2];
+        k2r a2[2], hh2[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            a2[i] = LL[i] * a.K2sq;
-            hh2[i] = HH[i] * a.invK2sq;
+            a2[i] = LL[i] * k2r(a.K2sq);
+            hh2[i] = HH[i] * k2r(a.invK2sq);
         }
-        const double hh2_l = shl(hh2[1]);
-        double lh2p[2], hl2p[2];
+        const k2r hh2_l = shl(hh2[1]);
+        k2r lh2p[2], hl2p[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            lh2p[i] = fma(-a.c3, hh2[i] + (i == 0 ? hh2_l : hh2[0]), LH[i]);
-            hl2p[i] = fma(-a.c3, hh2[i] + cy[i].hh2, HL[i]);
+            lh2p[i] = fma(-k2r(a.c3), hh2[i] + (i == 0 ? hh2_l : hh2[0]), LH[i]);
+            hl2p[i] = fma(-k2r(a.c3), hh2[i] + cy[i].hh2, HL[i]);
         }
-        const double hl2p_l = shl(hl2p[1]);
-        double ll1[2];
+        const k2r hl2p_l = shl(hl2p[1]);
+        k2r ll1[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
-            ll1[i] = fma(-a.c3, LH[i] + cy[i].lh, fma(-a.c3, hl2p[i] + (i == 0 ? hl2p_l : hl2p[0]), a2[i]));
+            ll1[i] = fma(-k2r(a.c3), LH[i] + cy[i].lh, fma(-k2r(a.c3), hl2p[i] + (i == 0 ? hl2p_l : hl2p[0]), a2[i]));
         // ---- undo P2 completes row n-1 (carried hl2p, lh2p, ll1, hh2 of row n-1)
-        double pll1[2];
+        k2r pll1[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) pll1[i] = cy[i].ll1;
-        const double ll1_r = shr(pll1[0]);
-        double hl1[2], lh1[2];
+        const k2r ll1_r = shr(pll1[0]);
+        k2r hl1[2], lh1[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            hl1[i] = fma(-a.c2, pll1[i] + (i == 0 ? pll1[1] : ll1_r), cy[i].hl2p);
-            lh1[i] = fma(-a.c2, pll1[i] + ll1[i], cy[i].lh2p);
+            hl1[i] = fma(-k2r(a.c2), pll1[i] + (i == 0 ? pll1[1] : ll1_r), cy[i].hl2p);
+            lh1[i] = fma(-k2r(a.c2), pll1[i] + ll1[i], cy[i].lh2p);
         }
-        const double lh1_r = shr(lh1[0]);
-        double hh1[2];
+        const k2r lh1_r = shr(lh1[0]);
+        k2r hh1[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
-            hh1[i] = fma(-a.c2, cy[i].hl2p + hl2p[i], fma(-a.c2, lh1[i] + (i == 0 ? lh1[1] : lh1_r), cy[i].hh2));
+            hh1[i] = fma(-k2r(a.c2), cy[i].hl2p + hl2p[i], fma(-k2r(a.c2), lh1[i] + (i == 0 ? lh1[1] : lh1_r), cy[i].hh2));
         // ---- undo U1, row n-1 (carried hh1, lh1 of row n-2)
-        const double hh1_l = shl(hh1[1]);
-        double lh1p[2], hl1p[2];
+        const k2r hh1_l = shl(hh1[1]);
+        k2r lh1p[2], hl1p[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            lh1p[i] = fma(-a.c1, hh1[i] + (i == 0 ? hh1_l : hh1[0]), lh1[i]);
-            hl1p[i] = fma(-a.c1, hh1[i] + cy[i].hh1, hl1[i]);
+            lh1p[i] = fma(-k2r(a.c1), hh1[i] + (i == 0 ? hh1_l : hh1[0]), lh1[i]);
+            hl1p[i] = fma(-k2r(a.c1), hh1[i] + cy[i].hh1, hl1[i]);
         }
-        const double hl1p_l = shl(hl1p[1]);
-        double av[2];
+        const k2r hl1p_l = shl(hl1p[1]);
+        k2r av[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
-            av[i] = fma(-a.c1, lh1[i] + cy[i].lh1, fma(-a.c1, hl1p[i] + (i == 0 ? hl1p_l : hl1p[0]), pll1[i]));
+            av[i] = fma(-k2r(a.c1), lh1[i] + cy[i].lh1, fma(-k2r(a.c1), hl1p[i] + (i == 0 ? hl1p_l : hl1p[0]), pll1[i]));
         // ---- undo P1 completes row n-2 (carried a, hl1p, lh1p, hh1 of row n-2)
-        double pa[2];
+        k2r pa[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) pa[i] = cy[i].a;
-        const double a_r = shr(pa[0]);
-        double bo[2], co[2];
+        const k2r a_r = shr(pa[0]);
+        k2r bo[2], co[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            bo[i] = fma(-a.c0, pa[i] + (i == 0 ? pa[1] : a_r), cy[i].hl1p);
-            co[i] = fma(-a.c0, pa[i] + av[i], cy[i].lh1p);
+            bo[i] = fma(-k2r(a.c0), pa[i] + (i == 0 ? pa[1] : a_r), cy[i].hl1p);
+            co[i] = fma(-k2r(a.c0), pa[i] + av[i], cy[i].lh1p);
         }
-        const double c_r = shr(co[0]);
-        double dout[2];
+        const k2r c_r = shr(co[0]);
+        k2r dout[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
-            dout[i] = fma(-a.c0, cy[i].hl1p + hl1p[i], fma(-a.c0, co[i] + (i == 0 ? co[1] : c_r), cy[i].hh1));
+            dout[i] = fma(-k2r(a.c0), cy[i].hl1p + hl1p[i], fma(-k2r(a.c0), co[i] + (i == 0 ? co[1] : c_r), cy[i].hh1));
         // ---- store pixel rows 2(n-2), 2(n-2)+1
         const int q = n - 2;
         if (q >= n0 && q < n1 && out_lane) {
