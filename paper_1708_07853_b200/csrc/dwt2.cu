@@ -1064,129 +1064,6 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
 #endif
 }
 
-__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned int *p)
-{
-    unsigned v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acquire.gpu;" ::: "memory"); }
-__device__ __forceinline__ void fence_release_gpu() { asm volatile("fence.release.gpu;" ::: "memory"); }
-
-__device__ __forceinline__ void red_relaxed_add(unsigned int *p, unsigned v)
-{
-    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// ---------------------------------------------------------------------------
-// Tail kernel: the small last levels of a forward (and small one-level
-// images) in ONE launch, a grid barrier between levels.  Levels of a few
-// hundred KB are latency-bound -- one dependent launch of the level kernel
-// costs ~4 us whatever its size (config 4's levels 4-8 take 21 us
-// for 1.5 % of the bytes).  Here every thread owns quads and evaluates each
-// quad's four coefficients pointwise from its 5 x 5 input neighbourhood: the
-// 2-D analysis filters of Eq. (4), which the lifting
-// steps of Eq. (5) reach exactly, as separable row / column passes over the
-// whole-sample-symmetric extension (h0 = (-1/8, 1/4, 3/4, 1/4, -1/8),
-// g1 = (-1/2, 1, -1/2)).  All 25 loads of a quad are independent (one L2
-// round trip instead of the level kernel's TMA / stage chain), fp64 in
-// registers as the level kernel: for these data every product and sum is
-// exact, so the stored fp32 is the correctly rounded exact coefficient, bit
-// for bit the level kernel's result.  One or two CTAs per SM, all resident,
-// so the grid barrier (release / acquire on a counter) is safe.
-// ---------------------------------------------------------------------------
-constexpr int TAIL_THREADS = 256;
-constexpr int MAX_TAIL = 16;
-
-struct TailLevel {
-    const float *in;
-    long long in_pitch, in_img;       // input rows and images (floats)
-    float *ll;
-    long long ll_pitch, ll_img;       // LL destination
-    float *out;
-    long long out_pitch, out_img;     // Mallat base of this level's HL / LH / HH
-    int W, H;
-};
-
-struct TailArgs {
-    TailLevel lv[MAX_TAIL];
-    int nlev, count;
-    unsigned int *bar;                // [0] barrier arrivals, [1] CTAs done (the last zeroes both)
-};
-
-__device__ __forceinline__ int wss_idx(int k, int n)
-{
-    // whole-sample symmetric reflection for k in [-2, n + 1], n >= 2
-    k = k < 0 ? -k : k;
-    return k >= n ? 2 * (n - 1) - k : k;
-}
-
-__device__ __forceinline__ void tail_barrier(unsigned int *bar, unsigned target)
-{
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        fence_release_gpu();
-        red_relaxed_add(bar, 1u);
-        while (ld_relaxed_u32(bar) < target) {}
-        fence_acquire_gpu();
-    }
-    __syncthreads();
-}
-
-__global__ void __launch_bounds__(TAIL_THREADS)
-dwt53_tail_kernel(const __grid_constant__ TailArgs ta)
-{
-    pdl_launch_dependents();
-    pdl_wait();
-    const long long nthr = (long long)gridDim.x * TAIL_THREADS;
-    const long long tid = (long long)blockIdx.x * TAIL_THREADS + threadIdx.x;
-    for (int k = 0; k < ta.nlev; ++k) {
-        if (k > 0) tail_barrier(ta.bar, unsigned(k) * gridDim.x);
-        const TailLevel &L = ta.lv[k];
-        const int W = L.W, H = L.H;
-        const int Wq = (W + 1) >> 1, Hq = (H + 1) >> 1, Wh = W >> 1, Hh = H >> 1;
-        const long long per_img = (long long)Wq * Hq;
-        const long long total = per_img * ta.count;
-        for (long long q = tid; q < total; q += nthr) {
-            const int img = int(q / per_img);
-            const int r = int(q - img * per_img);
-            const int n = r / Wq, m = r - n * Wq;
-            const float *x = L.in + img * L.in_img;
-            int cx[5];
-#pragma unroll
-            for (int i = 0; i < 5; ++i) cx[i] = wss_idx(2 * m - 2 + i, W);
-            real lo[5], hi[5];         // row passes: h0 at column 2m, g1 at column 2m + 1
-#pragma unroll
-            for (int j = 0; j < 5; ++j) {
-                const float *row = x + (long long)wss_idx(2 * n - 2 + j, H) * L.in_pitch;
-                real v[5];
-#pragma unroll
-                for (int i = 0; i < 5; ++i) v[i] = __ldcg(row + cx[i]);
-                lo[j] = fma(R_(0.75), v[2], fma(R_(0.25), v[1] + v[3], R_(-0.125) * (v[0] + v[4])));
-                hi[j] = fma(R_(-0.5), v[2] + v[4], v[3]);
-            }
-            const real ll = fma(R_(0.75), lo[2], fma(R_(0.25), lo[1] + lo[3], R_(-0.125) * (lo[0] + lo[4])));
-            const real lh = fma(R_(-0.5), lo[2] + lo[4], lo[3]);
-            const real hl = fma(R_(0.75), hi[2], fma(R_(0.25), hi[1] + hi[3], R_(-0.125) * (hi[0] + hi[4])));
-            const real hh = fma(R_(-0.5), hi[2] + hi[4], hi[3]);
-            L.ll[img * L.ll_img + (long long)n * L.ll_pitch + m] = to_f32(ll);
-            float *o = L.out + img * L.out_img;
-            if (m < Wh) o[(long long)n * L.out_pitch + Wq + m] = to_f32(hl);
-            if (n < Hh) {
-                o[(long long)(Hq + n) * L.out_pitch + m] = to_f32(lh);
-                if (m < Wh) o[(long long)(Hq + n) * L.out_pitch + Wq + m] = to_f32(hh);
-            }
-        }
-    }
-    // the last CTA out resets the barrier counters for the next launch
-    __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(ta.bar + 1, 1u) == gridDim.x - 1) {
-        atomicExch(ta.bar, 0u);
-        atomicExch(ta.bar + 1, 0u);
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
@@ -1623,73 +1500,27 @@ bool on_plan_device(const dwt2_plan *p, const void *ptr)
 
 namespace {
 
-// The small last levels of a forward as one tail launch (dwt53_tail_kernel).
+// The small last levels of a forward as one tail launch (tail.cu).
 int32_t launch_tail(const dwt2_plan *p, int first, int n, const LaunchIO *ios, cudaStream_t stream)
 {
-    if (n < 1 || n > MAX_TAIL) return fail(DWT2_EINVAL);
-    TailArgs ta;
-    memset(&ta, 0, sizeof(ta));
-    ta.nlev = n;
-    ta.count = ios[0].count;
-    long long most = 0;
+    TailLevelIO lv[MAX_TAIL];
     for (int k = 0; k < n; ++k) {
         const LevelGeom &g = p->geom[first + k];
         const LaunchIO &io = ios[k];
-        TailLevel &L = ta.lv[k];
-        L.in = io.in;
-        L.in_pitch = io.in_pitch;
-        L.in_img = io.in_img_stride;
-        L.ll = io.ll;
-        L.ll_pitch = io.ll_pitch;
-        L.ll_img = io.ll_img_stride;
-        L.out = io.out;
-        L.out_pitch = io.out_pitch;
-        L.out_img = io.out_img_stride;
-        L.W = g.W;
-        L.H = g.H;
-        most = std::max<long long>(most, (long long)g.Wq * g.Hq * io.count);
+        lv[k] = TailLevelIO{io.in, io.in_pitch, io.in_img_stride, io.ll, io.ll_pitch, io.ll_img_stride,
+                            io.out, io.out_pitch, io.out_img_stride, g.W, g.H};
     }
-    ta.bar = p->counters + 2 * QUEUE_TAIL;
-    // every CTA must be resident at once (grid barrier): at most the occupancy
-    static const int resident = [] {
-        int n = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dwt53_tail_kernel, TAIL_THREADS, 0) != cudaSuccess) n = 1;
-        cudaGetLastError();
-        return std::max(1, n);
-    }();
-    static const int per_sm = std::min(resident, tuning_int("DWT2_TAIL_CTAS", 2, 1, 8));
-    const long long want = (most + TAIL_THREADS - 1) / TAIL_THREADS;
-    const int grid = int(std::max<long long>(1, std::min<long long>((long long)p->sms * per_sm, want)));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(TAIL_THREADS);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, dwt53_tail_kernel, ta) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(DWT2_ECUDA);
-    }
-    return DWT2_OK;
+    return launch_tail_levels(p, lv, n, ios[0].count, tail_filter_53(), stream);
 }
 
-// First level of [first, last] from which every level fits the tail kernel
-// (at most tail_quads quads over all images; last + 1: none).
+// First level of [first, last] that starts the tail launch (last + 1: none).
 int tail_start(const dwt2_plan *p, int count, int first, int last)
 {
     // measured (config 4): levels of <= 256^2 input (16384 quads) 141.2 -> 140.5 us; adding the
     // 512^2 level changes nothing, adding 1024^2 is slower (145.4); a 512^2 one-level image (config 1)
     // is faster on the level kernel (3.9 vs 4.4 us per call)
     static const int tail_quads = tuning_int("DWT2_TAIL_QUADS", 1 << 14, 0, 1 << 30);
-    int k = last + 1;
-    while (k - 1 >= first && last - (k - 1) < MAX_TAIL &&
-           (long long)p->geom[k - 1].Wq * p->geom[k - 1].Hq * count <= tail_quads)
-        --k;
-    return k;
+    return tail_start_levels(p, count, first, last, tail_quads);
 }
 
 // Launch geometry of level k of a forward of `count` images: level 0 reads
@@ -2138,9 +1969,10 @@ int32_t dwt2_plan_info(const dwt2_plan *p, dwt2_plan_info_t *info)
     info->levels = p->levels;
     info->max_count = p->max_count;
     info->launches_per_forward = p->levels;
-    if (p->wavelet == DWT2_WAVELET_CDF53 && !p->strip) {
-        // the small last levels run as one tail launch (run_levels)
-        const int t0 = tail_start(p, p->max_count, 0, p->levels - 1);
+    if (!p->strip) {
+        // the small last levels run as one tail launch (run_levels, run_levels_k2)
+        const int t0 = p->wavelet == DWT2_WAVELET_CDF53 ? tail_start(p, p->max_count, 0, p->levels - 1)
+                                                        : k2_tail_start(p, p->max_count);
         if (t0 < p->levels) info->launches_per_forward = t0 + 1;
     }
     int tma = 0;

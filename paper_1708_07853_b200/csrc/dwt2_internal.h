@@ -129,6 +129,32 @@ struct dwt2_plan {
 
 namespace dwt2_detail {
 
+// ---- tail kernel (tail.cu): the small last levels of a forward in one launch
+constexpr int MAX_TAIL = 16;
+
+struct TailLevelIO {
+    const float *in;
+    long long in_pitch, in_img;       // level input rows and images (floats)
+    float *ll;
+    long long ll_pitch, ll_img;       // LL destination
+    float *out;
+    long long out_pitch, out_img;     // Mallat base of this level's HL / LH / HH
+    int W, H;                         // level input size (each >= 2)
+};
+
+struct TailFilter {
+    int radius;                       // 2: CDF 5/3 (exact path); 4: K <= 2 lifting filters below
+    double h[9], g[7];                // low taps at offsets -4..4, high taps at -3..3 (radius 4)
+    double sll, sd, shh;              // output scaling (radius 4)
+};
+
+TailFilter tail_filter_53();
+TailFilter tail_filter_from_lifting(double c0, double c1, double c2, double c3, double K);
+// first level of [first, last] from which every level has <= max_quads quads over `count` images
+int tail_start_levels(const dwt2_plan *p, int count, int first, int last, long long max_quads);
+int32_t launch_tail_levels(const dwt2_plan *p, const TailLevelIO *lv, int n, int count, const TailFilter &f,
+                           cudaStream_t stream);
+
 // true if ptr is device (or managed) memory of the plan's device
 bool on_plan_device(const dwt2_plan *p, const void *ptr);
 
@@ -140,6 +166,9 @@ int32_t forward_fused_variant(const dwt2_plan *p, const float *in, float *out, i
 // inverse of all levels through the K = 2 lifting kernel (dwt97.cu)
 int32_t run_inverse_k2(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,
                        long long out_stride, cudaStream_t s);
+
+// first level of a K = 2 forward that runs in the tail launch (levels: none)
+int k2_tail_start(const dwt2_plan *p, int count);
 
 // all levels through the K = 2 lifting kernel (dwt97.cu)
 int32_t run_levels_k2(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,

@@ -808,10 +808,21 @@ namespace dwt2_detail {
 
 // All levels of the K = 2 lifting kernel (plans created with a wavelet other
 // than DWT2_WAVELET_CDF53); buffer roles as run_levels in dwt2.cu.
+int k2_tail_start(const dwt2_plan *p, int count)
+{
+    static const int k2_tail_quads = tuning_int("DWT2_K2_TAIL_QUADS", 1 << 18, 0, 1 << 30);
+    return tail_start_levels(p, count, 0, p->levels - 1, k2_tail_quads);
+}
+
 int32_t run_levels_k2(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,
                       long long out_stride, cudaStream_t s)
 {
     const Wavelet2 wv = wavelet_params(p);
+    // the small last levels in one tail launch (tail.cu, radius-4 filters of the
+    // lifting pair): the K = 2 kernel walks a tile row by row through four
+    // lifting steps, ~9-20 us per dependent launch on a small level
+    const int t0 = k2_tail_start(p, count);
+    TailLevelIO tail[MAX_TAIL];
     for (int k = 0; k < p->levels; ++k) {
         const LevelGeom &g = p->geom[k];
         K2Args a;
@@ -848,10 +859,18 @@ int32_t run_levels_k2(const dwt2_plan *p, const float *in, float *out, int count
             a.ll_pitch = p->sc_pitch[si];
             a.ll_img = p->sc_img_stride[si];
         }
+        if (k >= t0) {
+            tail[k - t0] = TailLevelIO{a.in, a.in_pitch, a.in_img, a.ll, a.ll_pitch, a.ll_img,
+                                       out, a.out_pitch, a.out_img, a.W, a.H};
+            continue;
+        }
         a.counter = p->counters + 2 * (QUEUE_FORWARD + k);
         int32_t r = launch_k2_level(p, a, s);
         if (r != DWT2_OK) return r;
     }
+    if (t0 < p->levels)
+        return launch_tail_levels(p, tail, p->levels - t0, count,
+                                  tail_filter_from_lifting(wv.c0, wv.c1, wv.c2, wv.c3, wv.K), s);
     return DWT2_OK;
 }
 

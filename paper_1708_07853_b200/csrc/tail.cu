@@ -1,0 +1,278 @@
+// tail.cu -- the small last levels of a forward in ONE launch (SURVEY.md 8a
+// row a7, the multi-level driver; BASELINE.json north_star "a multi-level
+// driver recursing on LL").
+//
+// Levels of a few hundred KB are latency-bound: one dependent launch of a
+// level kernel costs ~3.5-4 us whatever its size for the 5/3 kernel and 9-20 us
+// for the K = 2 (CDF 9/7) kernel, whose warps walk a tile row by row through
+// four lifting steps.  The tail kernel runs every such level
+// in one launch of one or two CTAs per SM, all resident (the grid is clamped to
+// the kernel's occupancy), with a grid barrier (release / acquire on a
+// self-resetting counter) between levels.  Each thread owns quads and
+// evaluates a quad's four coefficients pointwise from its neighbourhood of the
+// whole-sample-symmetric extension: the 2-D analysis filters of Eq. (4)
+// -- which the lifting steps of Eq. (5) reach exactly --
+// as a row pass and a column pass:
+//
+//   LL = s_ll * h (x) h,  HL = s_d * g (x) h,  LH = s_d * h (x) g,  HH = s_hh * g (x) g
+//
+// with h the low-pass taps at even positions (radius R) and g the high-pass
+// taps at odd positions (radius R - 1).  R = 2: the CDF 5/3 pair, taps written
+// out (h = (-1/8, 1/4, 3/4, 1/4, -1/8), g = (-1/2, 1, -1/2)); every product
+// and sum is exact in fp64 for these data, so the stored fp32 is bit for bit
+// the level kernel's.  R = 4: any K <= 2 lifting pair (CDF 9/7, general
+// lifting plans), taps derived on the host from the lifting coefficients by
+// lifting unit impulses (tail_filter_from_lifting); the result differs from
+// the lifting order only by fp64 rounding (<< the 1e-4 bar).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "dwt2_internal.h"
+
+using namespace dwt2_detail;
+
+namespace {
+
+constexpr int TAIL_THREADS = 256;
+
+struct TailArgs {
+    TailLevelIO lv[MAX_TAIL];
+    double h[9], g[7];                // R = 4 taps, index = offset + 4 (h) / + 3 (g)
+    double sll, sd, shh;              // output scaling (R = 4)
+    int nlev, count;
+    unsigned int *bar;                // [0] barrier arrivals, [1] CTAs done (the last zeroes both)
+};
+
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned int *p)
+{
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void tail_barrier(unsigned int *bar, unsigned target)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("fence.release.gpu;" ::: "memory");
+        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        while (ld_relaxed(bar) < target) {}
+        asm volatile("fence.acquire.gpu;" ::: "memory");
+    }
+    __syncthreads();
+}
+
+// whole-sample symmetric reflection, any k (period 2 (n - 1), n >= 2)
+__device__ __forceinline__ int wss_any(int k, int n)
+{
+    const int p = 2 * (n - 1);
+    k %= p;
+    if (k < 0) k += p;
+    return k >= n ? p - k : k;
+}
+
+// reflection for k in [-2, n + 1], n >= 2 (radius-2 path)
+__device__ __forceinline__ int wss2(int k, int n)
+{
+    k = k < 0 ? -k : k;
+    return k >= n ? 2 * (n - 1) - k : k;
+}
+
+template <int R>
+__global__ void __launch_bounds__(TAIL_THREADS) dwt_tail_kernel(const __grid_constant__ TailArgs ta)
+{
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    constexpr int NT = 2 * R + 1;     // taps of h (g: NT - 2)
+    const long long nthr = (long long)gridDim.x * TAIL_THREADS;
+    const long long tid = (long long)blockIdx.x * TAIL_THREADS + threadIdx.x;
+    for (int k = 0; k < ta.nlev; ++k) {
+        if (k > 0) tail_barrier(ta.bar, unsigned(k) * gridDim.x);
+        const TailLevelIO &L = ta.lv[k];
+        const int W = L.W, H = L.H;
+        const int Wq = (W + 1) >> 1, Hq = (H + 1) >> 1, Wh = W >> 1, Hh = H >> 1;
+        const long long per_img = (long long)Wq * Hq;
+        const long long total = per_img * ta.count;
+        for (long long q = tid; q < total; q += nthr) {
+            const int img = int(q / per_img);
+            const int r = int(q - img * per_img);
+            const int n = r / Wq, m = r - n * Wq;
+            const float *x = L.in + img * L.in_img;
+            int cx[NT];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) cx[i] = R == 2 ? wss2(2 * m - R + i, W) : wss_any(2 * m - R + i, W);
+            double lo[NT], hi[NT];     // row passes: h at column 2m, g at column 2m + 1
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                const int y = R == 2 ? wss2(2 * n - R + j, H) : wss_any(2 * n - R + j, H);
+                const float *row = x + (long long)y * L.in_pitch;
+                double v[NT];
+#pragma unroll
+                for (int i = 0; i < NT; ++i) v[i] = __ldcg(row + cx[i]);
+                if (R == 2) {
+                    lo[j] = fma(0.75, v[2], fma(0.25, v[1] + v[3], -0.125 * (v[0] + v[4])));
+                    hi[j] = fma(-0.5, v[2] + v[4], v[3]);
+                } else {
+                    double s = 0.0, t = 0.0;
+#pragma unroll
+                    for (int i = 0; i < NT; ++i) s = fma(ta.h[i], v[i], s);
+#pragma unroll
+                    for (int i = 0; i < NT - 2; ++i) t = fma(ta.g[i], v[i + 2], t);
+                    lo[j] = s;
+                    hi[j] = t;
+                }
+            }
+            double ll, lh, hl, hh;
+            if (R == 2) {
+                ll = fma(0.75, lo[2], fma(0.25, lo[1] + lo[3], -0.125 * (lo[0] + lo[4])));
+                lh = fma(-0.5, lo[2] + lo[4], lo[3]);
+                hl = fma(0.75, hi[2], fma(0.25, hi[1] + hi[3], -0.125 * (hi[0] + hi[4])));
+                hh = fma(-0.5, hi[2] + hi[4], hi[3]);
+            } else {
+                ll = lh = hl = hh = 0.0;
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    ll = fma(ta.h[j], lo[j], ll);
+                    hl = fma(ta.h[j], hi[j], hl);
+                }
+#pragma unroll
+                for (int j = 0; j < NT - 2; ++j) {
+                    lh = fma(ta.g[j], lo[j + 2], lh);
+                    hh = fma(ta.g[j], hi[j + 2], hh);
+                }
+                ll *= ta.sll;
+                hl *= ta.sd;
+                lh *= ta.sd;
+                hh *= ta.shh;
+            }
+            L.ll[img * L.ll_img + (long long)n * L.ll_pitch + m] = (float)ll;
+            float *o = L.out + img * L.out_img;
+            if (m < Wh) o[(long long)n * L.out_pitch + Wq + m] = (float)hl;
+            if (n < Hh) {
+                o[(long long)(Hq + n) * L.out_pitch + m] = (float)lh;
+                if (m < Wh) o[(long long)(Hq + n) * L.out_pitch + Wq + m] = (float)hh;
+            }
+        }
+    }
+    // the last CTA out resets the barrier counters for the next launch
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(ta.bar + 1, 1u) == gridDim.x - 1) {
+        atomicExch(ta.bar, 0u);
+        atomicExch(ta.bar + 1, 0u);
+    }
+}
+
+template <int R>
+int tail_resident()
+{
+    static int n = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dwt_tail_kernel<R>, TAIL_THREADS, 0) != cudaSuccess)
+            n = 1;
+        n = std::max(1, n);
+    });
+    cudaGetLastError();
+    return n;
+}
+
+}  // namespace
+
+namespace dwt2_detail {
+
+TailFilter tail_filter_53()
+{
+    TailFilter f;
+    memset(&f, 0, sizeof(f));
+    f.radius = 2;
+    f.sll = f.sd = f.shh = 1.0;
+    return f;
+}
+
+TailFilter tail_filter_from_lifting(double c0, double c1, double c2, double c3, double K)
+{
+    // 1-D lifting of a unit impulse at position p of a long signal, far from
+    // its ends: low[i] = h[p - 2 i], high[i] = g[p - 2 i - 1]
+    //   d1 = x_odd + c0 (x_even[i] + x_even[i+1]),  s1 = x_even + c1 (d1[i-1] + d1[i]),
+    //   d2 = d1 + c2 (s1[i] + s1[i+1]),             s2 = s1 + c3 (d2[i-1] + d2[i])
+    TailFilter f;
+    memset(&f, 0, sizeof(f));
+    f.radius = 4;
+    constexpr int N = 64, M = N / 2;
+    for (int p = 30; p <= 31; ++p) {
+        double x[N] = {0};
+        x[p] = 1.0;
+        double s[M], d[M];
+        for (int i = 0; i < M; ++i) d[i] = x[2 * i + 1] + c0 * (x[2 * i] + (2 * i + 2 < N ? x[2 * i + 2] : 0.0));
+        for (int i = 0; i < M; ++i) s[i] = x[2 * i] + c1 * ((i > 0 ? d[i - 1] : 0.0) + d[i]);
+        for (int i = 0; i < M; ++i) d[i] = d[i] + c2 * (s[i] + (i + 1 < M ? s[i + 1] : 0.0));
+        for (int i = 0; i < M; ++i) s[i] = s[i] + c3 * ((i > 0 ? d[i - 1] : 0.0) + d[i]);
+        for (int i = 0; i < M; ++i) {
+            const int jl = p - 2 * i, jh = p - 2 * i - 1;
+            if (jl >= -4 && jl <= 4) f.h[jl + 4] = s[i];
+            if (jh >= -3 && jh <= 3) f.g[jh + 3] = d[i];
+        }
+    }
+    // 2-D scaling (JPEG 2000 normalisation, DESIGN.md C-B2): low / K and high * K per axis
+    f.sll = 1.0 / (K * K);
+    f.sd = 1.0;
+    f.shh = K * K;
+    return f;
+}
+
+int tail_start_levels(const dwt2_plan *p, int count, int first, int last, long long max_quads)
+{
+    int k = last + 1;
+    while (k - 1 >= first && last - (k - 1) < MAX_TAIL &&
+           (long long)p->geom[k - 1].Wq * p->geom[k - 1].Hq * count <= max_quads)
+        --k;
+    return k;
+}
+
+int32_t launch_tail_levels(const dwt2_plan *p, const TailLevelIO *lv, int n, int count, const TailFilter &f,
+                           cudaStream_t stream)
+{
+    if (n < 1 || n > MAX_TAIL || (f.radius != 2 && f.radius != 4)) return fail(DWT2_EINVAL);
+    TailArgs ta;
+    memset(&ta, 0, sizeof(ta));
+    ta.nlev = n;
+    ta.count = count;
+    long long most = 0;
+    for (int k = 0; k < n; ++k) {
+        ta.lv[k] = lv[k];
+        most = std::max<long long>(most, (long long)((lv[k].W + 1) / 2) * ((lv[k].H + 1) / 2) * count);
+    }
+    memcpy(ta.h, f.h, sizeof(ta.h));
+    memcpy(ta.g, f.g, sizeof(ta.g));
+    ta.sll = f.sll;
+    ta.sd = f.sd;
+    ta.shh = f.shh;
+    ta.bar = p->counters + 2 * QUEUE_TAIL;
+    // every CTA must be resident at once (grid barrier): at most the occupancy
+    const int resident = f.radius == 2 ? tail_resident<2>() : tail_resident<4>();
+    static const int per_sm_knob = tuning_int("DWT2_TAIL_CTAS", 2, 1, 8);
+    const int per_sm = std::min(resident, per_sm_knob);
+    const long long want = (most + TAIL_THREADS - 1) / TAIL_THREADS;
+    const int grid = int(std::max<long long>(1, std::min<long long>((long long)p->sms * per_sm, want)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(TAIL_THREADS);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = f.radius == 2 ? cudaLaunchKernelEx(&cfg, dwt_tail_kernel<2>, ta)
+                                        : cudaLaunchKernelEx(&cfg, dwt_tail_kernel<4>, ta);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DWT2_ECUDA);
+    }
+    return DWT2_OK;
+}
+
+}  // namespace dwt2_detail

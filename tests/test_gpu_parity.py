@@ -131,6 +131,19 @@ def test_config3_16384_sampled():
     assert np.abs(got).max() <= 1020
 
 
+def test_config3_16384_every_element():
+    """Config 3 at full size, EVERY element of the Mallat output against the
+    fp64 separable-lifting oracle (algorithm A) rounded to fp32 (oracle (ii)):
+    bit for bit (integer inputs: the exact coefficient is representable).
+    The oracle alone takes ~20 s and ~4.3 GB of host memory here."""
+    cfg = workloads.CONFIGS["3"]
+    x = cfg.groups[0].image(0)
+    got = gpu_forward(x, 1)
+    ref = oracle.forward(x.astype(np.float64), 1, round_f32=True)
+    d = got.astype(np.float64) != ref
+    assert not d.any(), f"{int(d.sum())} of {d.size} elements differ"
+
+
 @pytest.mark.parametrize("W,H", [(16384, 8192), (20000, 6001), (20001, 6001)])
 def test_large_level_tiles_sampled(W, H):
     """Levels large enough for the 15-row tile rule (tile_policy: >= 9 tiles

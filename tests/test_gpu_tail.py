@@ -77,3 +77,32 @@ def test_plan_info_counts_the_tail_launch():
     p = dwt2.Plan(512, 512, 1)
     assert p.info().launches_per_forward == 1
     p.close()
+
+
+@pytest.mark.parametrize("W,H", [(2, 2), (3, 5), (64, 64), (255, 257), (1025, 1023)])
+def test_tail_k2_cdf97_within_tolerance(W, H):
+    """CDF 9/7 plans: the small levels run in the tail kernel with the radius-4
+    filters derived from the lifting pair on the host; every level count
+    against the fp64 oracle (i) within BASELINE's 1e-4."""
+    x = workloads.uniform_real(W, H, W + 7 * H)
+    for L in range(1, _levels_max(W, H) + 1):
+        plan = dwt2.Plan(W, H, L, wavelet="cdf97")
+        got = plan.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+        plan.close()
+        ref = oracle.forward(x.astype(np.float64), L, round_f32=False, wavelet="cdf97")
+        assert np.abs(got - ref).max() <= 1e-4, f"{W}x{H} L{L}"
+
+
+def test_tail_k2_with_53_pair_bit_identical():
+    """The K = 2 path with the CDF 5/3 pair (its tail uses the radius-4 filters
+    derived from (-1/2, 1/4, 0, 0), dyadic taps, exact) equals the 5/3 product
+    path bit for bit, on a pyramid that ends in the tail."""
+    W, H, L = 777, 513, 7
+    x = workloads.uniform_real(W, H, 5)
+    p53 = dwt2.Plan(W, H, L)
+    pk2 = dwt2.Plan(W, H, L, wavelet="cdf53_k2")
+    a = p53.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    b = pk2.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    p53.close()
+    pk2.close()
+    np.testing.assert_array_equal(a, b)
