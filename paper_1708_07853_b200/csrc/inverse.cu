@@ -607,7 +607,32 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
 int32_t run_inverse(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,
                     long long out_stride, cudaStream_t s)
 {
-    for (int k = p->levels - 1; k >= 0; --k) {
+    // the small coarsest levels in one inverse-tail launch (tail.cu), then the
+    // level kernels for the rest
+    static const int itail_quads = tuning_int("DWT2_ITAIL_QUADS", 1 << 14, 0, 1 << 30);   // config 4: 177.7 -> 174.7 us
+    const int t = itail_end(p, count, itail_quads);
+    if (t < p->levels) {
+        ITailLevelIO lv[MAX_TAIL];
+        for (int k = p->levels - 1; k >= t; --k) {
+            const LevelGeom &g = p->geom[k];
+            ITailLevelIO &L = lv[p->levels - 1 - k];
+            L.ll = k == p->levels - 1 ? in : p->scratch[k % 2];
+            L.ll_pitch = k == p->levels - 1 ? p->W : p->sc_pitch[k % 2];
+            L.ll_img = k == p->levels - 1 ? in_stride : p->sc_img_stride[k % 2];
+            L.d = in;
+            L.d_pitch = p->W;
+            L.d_img = in_stride;
+            L.out = k == 0 ? out : p->scratch[(k - 1) % 2];
+            L.out_pitch = k == 0 ? p->W : p->sc_pitch[(k - 1) % 2];
+            L.out_img = k == 0 ? out_stride : p->sc_img_stride[(k - 1) % 2];
+            L.W = g.W;
+            L.H = g.H;
+        }
+        int32_t r = launch_itail_levels(p, lv, p->levels - t, count,
+                                        itail_filter_from_lifting(-0.5, 0.25, 0.0, 0.0, 1.0), s);
+        if (r != DWT2_OK) return r;
+    }
+    for (int k = t - 1; k >= 0; --k) {
         const LevelGeom &g = p->geom[k];
         InvArgs a;
         memset(&a, 0, sizeof(a));

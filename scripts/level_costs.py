@@ -14,6 +14,7 @@ W = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 H = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
 Lmax = int(sys.argv[3]) if len(sys.argv) > 3 else 8
 WAV = sys.argv[4] if len(sys.argv) > 4 else "cdf53"
+OP = sys.argv[5] if len(sys.argv) > 5 else "forward"
 K = 20
 x = torch.from_numpy(workloads.smooth_noise(W, H, 4) if hasattr(workloads, "smooth_noise")
                      else workloads.GENERATORS["smooth"](W, H, 4)).cuda()
@@ -23,7 +24,11 @@ prev = 0.0
 w, h = W, H
 for L in range(1, Lmax + 1):
     p = dwt2.Plan(W, H, L, wavelet=WAV)
-    us = time_calls(lambda q: p.forward(q[0], q[1]), pairs, K)
+    if OP == "inverse":
+        ipairs = [(p.forward(q[0]).clone(), q[1]) for q in pairs]
+        us = time_calls(lambda q: p.inverse(q[0], q[1]), ipairs, K)
+    else:
+        us = time_calls(lambda q: p.forward(q[0], q[1]), pairs, K)
     print(f"L={L}: {us:8.2f} us total, level {L} ({w}x{h}, {8 * w * h / 1e6:7.2f} MB): +{us - prev:6.2f} us")
     prev = us
     w, h = (w + 1) // 2, (h + 1) // 2
