@@ -441,6 +441,12 @@ int32_t launch_k2_level(const dwt2_plan *p, K2Args a, cudaStream_t s)
     long long tb = slab_rows / (tpw * warps);
     static const int min_tb = tuning_int("DWT2_K2_MINTB", 16, 4, 512);
     tb = std::max<long long>(min_tb, std::min<long long>(512, tb)); // 4 warm-up rows per tile: >= 16 rows
+    // levels with less than one minimum tile per resident warp: one tile per
+    // warp of ceil(rows / warps) (>= 4) rows, so every warp takes part (a
+    // small level is latency-bound: its time is one tile's row walk)
+    static const int small_f = tuning_int("DWT2_K2_SMALLF", 1, 0, 64);
+    if (slab_rows < (long long)min_tb * warps * small_f)
+        tb = std::max<long long>(4, (slab_rows + warps - 1) / warps);
     a.tb = int(tb);
     a.nblk = int((Hq + tb - 1) / tb);
     a.ntiles = (long long)a.count * a.nblk * a.nslabs;
@@ -810,7 +816,7 @@ namespace dwt2_detail {
 // than DWT2_WAVELET_CDF53); buffer roles as run_levels in dwt2.cu.
 int k2_tail_start(const dwt2_plan *p, int count)
 {
-    static const int k2_tail_quads = tuning_int("DWT2_K2_TAIL_QUADS", 1 << 18, 0, 1 << 30);
+    static const int k2_tail_quads = tuning_int("DWT2_K2_TAIL_QUADS", 1 << 16, 0, 1 << 30);
     return tail_start_levels(p, count, 0, p->levels - 1, k2_tail_quads);
 }
 
