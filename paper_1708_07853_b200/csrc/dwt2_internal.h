@@ -155,27 +155,6 @@ int tail_start_levels(const dwt2_plan *p, int count, int first, int last, long l
 int32_t launch_tail_levels(const dwt2_plan *p, const TailLevelIO *lv, int n, int count, const TailFilter &f,
                            cudaStream_t stream);
 
-struct ITailLevelIO {
-    const float *ll;
-    long long ll_pitch, ll_img;       // the level's LL (coarsest: the Mallat buffer; else the finer inverse's input)
-    const float *d;
-    long long d_pitch, d_img;         // the Mallat buffer holding the level's HL / LH / HH
-    float *out;
-    long long out_pitch, out_img;     // the reconstructed level input
-    int W, H;
-};
-
-struct ITailFilter {
-    int radius;                       // 2 or 4
-    double s0[9], s1[9];              // low / high synthesis taps at offsets -4..4
-    double kll, kd, khh;              // undo of the forward scaling, per subband
-};
-
-ITailFilter itail_filter_from_lifting(double c0, double c1, double c2, double c3, double K);
-int32_t launch_itail_levels(const dwt2_plan *p, const ITailLevelIO *lv, int n, int count, const ITailFilter &f,
-                            cudaStream_t stream);
-int itail_end(const dwt2_plan *p, int count, long long max_quads);
-
 // true if ptr is device (or managed) memory of the plan's device
 bool on_plan_device(const dwt2_plan *p, const void *ptr);
 

@@ -779,6 +779,9 @@ int32_t launch_k2_inverse_level(const dwt2_plan *p, K2InvArgs a, cudaStream_t s)
     // against the tpw-derived height; smaller levels keep it)
     static const int tb_large = tuning_int("DWT2_K2INV_TB", 20, 0, 512);
     if (tb_large > 0 && slab_rows >= 64 * warps) tb = tb_large;
+    // small levels: one short tile per warp (as the forward, launch_k2_level)
+    static const int small_f = tuning_int("DWT2_K2INV_SMALLF", 1, 0, 64);
+    if (slab_rows < (long long)min_tb * warps * small_f) tb = std::max<long long>(4, (slab_rows + warps - 1) / warps);
     a.tb = int(tb);
     a.nblk = int((Hq + tb - 1) / tb);
     a.ntiles = (long long)a.count * a.nblk * a.nslabs;
@@ -886,32 +889,7 @@ int32_t run_inverse_k2(const dwt2_plan *p, const float *in, float *out, int coun
                        long long out_stride, cudaStream_t s)
 {
     const Wavelet2 wv = wavelet_params(p);
-    // the small coarsest levels in one inverse-tail launch (tail.cu, synthesis
-    // taps of the lifting pair), then the K = 2 inverse kernel for the rest
-    static const int k2_itail_quads = tuning_int("DWT2_K2_ITAIL_QUADS", 1 << 16, 0, 1 << 30);   // 9/7 config 4: 320.1 -> 286.1 us
-    const int t = itail_end(p, count, k2_itail_quads);
-    if (t < p->levels) {
-        ITailLevelIO lv[MAX_TAIL];
-        for (int k = p->levels - 1; k >= t; --k) {
-            const LevelGeom &g = p->geom[k];
-            ITailLevelIO &L = lv[p->levels - 1 - k];
-            L.ll = k == p->levels - 1 ? in : p->scratch[k % 2];
-            L.ll_pitch = k == p->levels - 1 ? p->W : p->sc_pitch[k % 2];
-            L.ll_img = k == p->levels - 1 ? in_stride : p->sc_img_stride[k % 2];
-            L.d = in;
-            L.d_pitch = p->W;
-            L.d_img = in_stride;
-            L.out = k == 0 ? out : p->scratch[(k - 1) % 2];
-            L.out_pitch = k == 0 ? p->W : p->sc_pitch[(k - 1) % 2];
-            L.out_img = k == 0 ? out_stride : p->sc_img_stride[(k - 1) % 2];
-            L.W = g.W;
-            L.H = g.H;
-        }
-        int32_t r = launch_itail_levels(p, lv, p->levels - t, count,
-                                        itail_filter_from_lifting(wv.c0, wv.c1, wv.c2, wv.c3, wv.K), s);
-        if (r != DWT2_OK) return r;
-    }
-    for (int k = t - 1; k >= 0; --k) {
+    for (int k = p->levels - 1; k >= 0; --k) {
         const LevelGeom &g = p->geom[k];
         K2InvArgs a;
         memset(&a, 0, sizeof(a));

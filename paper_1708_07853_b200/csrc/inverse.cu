@@ -508,6 +508,10 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
         const int tpw = env_tpw > 0 ? env_tpw : (slab_rows >= 256 * rwarps ? 16 : 4);
         long long tb = slab_rows / (tpw * rwarps);
         tb = std::max<long long>(8, std::min<long long>(256, tb));
+        // small levels (fewer than one 8-row tile per resident warp): one
+        // short tile per warp, so every warp takes part
+        static const int small_inv = tuning_int("DWT2_INV_SMALL", 1, 0, 1);
+        if (small_inv && slab_rows < 8 * rwarps) tb = std::max<long long>(2, (slab_rows + rwarps - 1) / rwarps);
         // levels with >= 64 quad rows per warp: 20-row tiles (measured over
         // 8192^2 .. 16384^2 against 8, 12, 16, 24, 27..55-row tiles and the
         // guided split: 16384 x 8192 0.80 -> 0.88, 16384^2 0.89 -> 0.91,
@@ -607,32 +611,7 @@ int32_t launch_inverse_level(const dwt2_plan *p, const InvArgs &base, cudaStream
 int32_t run_inverse(const dwt2_plan *p, const float *in, float *out, int count, long long in_stride,
                     long long out_stride, cudaStream_t s)
 {
-    // the small coarsest levels in one inverse-tail launch (tail.cu), then the
-    // level kernels for the rest
-    static const int itail_quads = tuning_int("DWT2_ITAIL_QUADS", 1 << 14, 0, 1 << 30);   // config 4: 177.7 -> 174.7 us
-    const int t = itail_end(p, count, itail_quads);
-    if (t < p->levels) {
-        ITailLevelIO lv[MAX_TAIL];
-        for (int k = p->levels - 1; k >= t; --k) {
-            const LevelGeom &g = p->geom[k];
-            ITailLevelIO &L = lv[p->levels - 1 - k];
-            L.ll = k == p->levels - 1 ? in : p->scratch[k % 2];
-            L.ll_pitch = k == p->levels - 1 ? p->W : p->sc_pitch[k % 2];
-            L.ll_img = k == p->levels - 1 ? in_stride : p->sc_img_stride[k % 2];
-            L.d = in;
-            L.d_pitch = p->W;
-            L.d_img = in_stride;
-            L.out = k == 0 ? out : p->scratch[(k - 1) % 2];
-            L.out_pitch = k == 0 ? p->W : p->sc_pitch[(k - 1) % 2];
-            L.out_img = k == 0 ? out_stride : p->sc_img_stride[(k - 1) % 2];
-            L.W = g.W;
-            L.H = g.H;
-        }
-        int32_t r = launch_itail_levels(p, lv, p->levels - t, count,
-                                        itail_filter_from_lifting(-0.5, 0.25, 0.0, 0.0, 1.0), s);
-        if (r != DWT2_OK) return r;
-    }
-    for (int k = t - 1; k >= 0; --k) {
+    for (int k = p->levels - 1; k >= 0; --k) {
         const LevelGeom &g = p->geom[k];
         InvArgs a;
         memset(&a, 0, sizeof(a));

@@ -165,132 +165,6 @@ __global__ void __launch_bounds__(TAIL_THREADS) dwt_tail_kernel(const __grid_con
     }
 }
 
-// ---------------------------------------------------------------------------
-// Inverse tail: the small coarsest levels of an inverse (they come FIRST, the
-// coarsest one first) in one launch, a grid barrier between levels.  Each
-// thread owns output quads (pixel rows 2n, 2n+1, columns 2m, 2m+1) and
-// evaluates them pointwise by 2-D synthesis of the interleaved coefficient
-// field: c(y, x) = LL / HL / LH / HH by the parities of (y, x), at whole-
-// sample-symmetric mirrored positions (the coefficient field of a symmetric
-// input is symmetric in the interleaved index: H[-1] = H[0], H[M] = H[M-1],
-// L[M] = L[M-1] of the level kernels), and
-//   x(p_y, p_x) = sum_{q_y, q_x} s_{q_y mod 2}[p_y - q_y] s_{q_x mod 2}[p_x - q_x] k(q) c(q_y, q_x)
-// with s_0 / s_1 the low / high synthesis taps (radius <= R) and k the undo
-// of the forward scaling.  The taps are the inverse lifting applied to unit
-// impulses (itail_filter_*): CDF 5/3 s_0 = (1/2, 1, 1/2), s_1 = (-1/8, -1/4,
-// 3/4, -1/4, -1/8), dyadic, so fp64 evaluation is exact and the result is bit
-// for bit the inverse level kernel's (and oracle (ii)'s).
-// ---------------------------------------------------------------------------
-struct ITailArgs {
-    ITailLevelIO lv[MAX_TAIL];
-    double s0[9], s1[9];              // synthesis taps at offsets -4..4 (index offset + 4)
-    double kll, kd, khh;              // coefficient scaling before synthesis
-    int nlev, count;
-    unsigned int *bar;
-};
-
-template <int R>
-__global__ void __launch_bounds__(TAIL_THREADS) dwt_itail_kernel(const __grid_constant__ ITailArgs ta)
-{
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    constexpr int WS = 2 * R + 2;     // coefficient rows / columns a quad's 2 x 2 pixels need
-    const long long nthr = (long long)gridDim.x * TAIL_THREADS;
-    const long long tid = (long long)blockIdx.x * TAIL_THREADS + threadIdx.x;
-    for (int k = 0; k < ta.nlev; ++k) {
-        if (k > 0) tail_barrier(ta.bar, unsigned(k) * gridDim.x);
-        const ITailLevelIO &L = ta.lv[k];
-        const int W = L.W, H = L.H;
-        const int Wq = (W + 1) >> 1, Hq = (H + 1) >> 1;
-        const long long per_img = (long long)Wq * Hq;
-        const long long total = per_img * ta.count;
-        for (long long q = tid; q < total; q += nthr) {
-            const int img = int(q / per_img);
-            const int r = int(q - img * per_img);
-            const int n = r / Wq, m = r - n * Wq;
-            const float *llp = L.ll + img * L.ll_img;
-            const float *dp = L.d + img * L.d_img;
-            int cx[WS], px[WS];
-#pragma unroll
-            for (int i = 0; i < WS; ++i) {
-                const int x = wss_any(2 * m - R + i, W);
-                cx[i] = x >> 1;
-                px[i] = x & 1;
-            }
-            // every coefficient of the window first (independent loads: one
-            // L2 round trip), then the separable synthesis
-            float v[WS][WS];
-            int pyj[WS];
-#pragma unroll
-            for (int j = 0; j < WS; ++j) {
-                const int y = wss_any(2 * n - R + j, H);
-                const int ry = y >> 1, py = y & 1;
-                pyj[j] = py;
-                const float *lrow = llp + (long long)ry * L.ll_pitch;
-                const float *drow = dp + (long long)(py ? Hq + ry : ry) * L.d_pitch;
-#pragma unroll
-                for (int i = 0; i < WS; ++i) {
-                    const float *src = (!py && !px[i]) ? lrow + cx[i] : drow + (px[i] ? Wq + cx[i] : cx[i]);
-                    v[j][i] = __ldcg(src);
-                }
-            }
-            double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-            for (int j = 0; j < WS; ++j) {
-                const int py = pyj[j];
-                // horizontal synthesis of coefficient row j to the quad's two columns
-                double h0 = 0.0, h1 = 0.0;
-#pragma unroll
-                for (int i = 0; i < WS; ++i) {
-                    const int qpar = (R + i) & 1;              // parity of column 2m - R + i
-                    const double k = (!py && !px[i]) ? ta.kll : (py && px[i]) ? ta.khh : ta.kd;
-                    const double c = k * double(v[j][i]);
-                    const double *sx = qpar ? ta.s1 : ta.s0;
-                    const int o0 = R - i;                      // (2m - (2m - R + i))
-                    if (o0 >= -4 && o0 <= 4) h0 = fma(sx[o0 + 4], c, h0);
-                    if (o0 + 1 >= -4 && o0 + 1 <= 4) h1 = fma(sx[o0 + 5], c, h1);
-                }
-                const double *sy = ((R + j) & 1) ? ta.s1 : ta.s0;
-                const int o0 = R - j;
-                if (o0 >= -4 && o0 <= 4) {
-                    acc[0][0] = fma(sy[o0 + 4], h0, acc[0][0]);
-                    acc[0][1] = fma(sy[o0 + 4], h1, acc[0][1]);
-                }
-                if (o0 + 1 >= -4 && o0 + 1 <= 4) {
-                    acc[1][0] = fma(sy[o0 + 5], h0, acc[1][0]);
-                    acc[1][1] = fma(sy[o0 + 5], h1, acc[1][1]);
-                }
-            }
-            float *o = L.out + img * L.out_img + (long long)(2 * n) * L.out_pitch + 2 * m;
-            o[0] = (float)acc[0][0];
-            if (2 * m + 1 < W) o[1] = (float)acc[0][1];
-            if (2 * n + 1 < H) {
-                o[L.out_pitch] = (float)acc[1][0];
-                if (2 * m + 1 < W) o[L.out_pitch + 1] = (float)acc[1][1];
-            }
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(ta.bar + 1, 1u) == gridDim.x - 1) {
-        atomicExch(ta.bar, 0u);
-        atomicExch(ta.bar + 1, 0u);
-    }
-}
-
-template <int R>
-int itail_resident()
-{
-    static int n = 0;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dwt_itail_kernel<R>, TAIL_THREADS, 0) != cudaSuccess)
-            n = 1;
-        n = std::max(1, n);
-    });
-    cudaGetLastError();
-    return n;
-}
-
 template <int R>
 int tail_resident()
 {
@@ -399,94 +273,6 @@ int32_t launch_tail_levels(const dwt2_plan *p, const TailLevelIO *lv, int n, int
         return fail(DWT2_ECUDA);
     }
     return DWT2_OK;
-}
-
-ITailFilter itail_filter_from_lifting(double c0, double c1, double c2, double c3, double K)
-{
-    // inverse 1-D lifting of a unit coefficient at interleaved position q
-    // (even: low, odd: high) of a long signal, far from its ends:
-    //   s1 = s2 - c3 (d2[i-1] + d2[i]),  d1 = d2 - c2 (s1[i] + s1[i+1]),
-    //   x_even = s1 - c1 (d1[i-1] + d1[i]),  x_odd = d1 - c0 (x_even[i] + x_even[i+1])
-    ITailFilter f;
-    memset(&f, 0, sizeof(f));
-    constexpr int N = 64, M = N / 2;
-    for (int q = 30; q <= 31; ++q) {
-        double s[M] = {0}, d[M] = {0}, x[N];
-        if (q % 2 == 0) s[q / 2] = 1.0;
-        else d[q / 2] = 1.0;
-        for (int i = 0; i < M; ++i) s[i] = s[i] - c3 * ((i > 0 ? d[i - 1] : 0.0) + d[i]);
-        for (int i = 0; i < M; ++i) d[i] = d[i] - c2 * (s[i] + (i + 1 < M ? s[i + 1] : 0.0));
-        for (int i = 0; i < M; ++i) x[2 * i] = s[i] - c1 * ((i > 0 ? d[i - 1] : 0.0) + d[i]);
-        for (int i = 0; i < M; ++i) x[2 * i + 1] = d[i] - c0 * (x[2 * i] + (2 * i + 2 < N ? x[2 * i + 2] : 0.0));
-        double *tap = q % 2 == 0 ? f.s0 : f.s1;
-        int reach = 0;
-        for (int p = 0; p < N; ++p) {
-            const int off = p - q;
-            if (off >= -4 && off <= 4) tap[off + 4] = x[p];
-            else if (x[p] != 0.0) reach = 5;
-            if (x[p] != 0.0) reach = std::max(reach, off < 0 ? -off : off);
-        }
-        f.radius = std::max(f.radius, reach);
-    }
-    f.radius = f.radius <= 2 ? 2 : 4;
-    // undo the forward scaling (LL / K^2, HL and LH * 1, HH * K^2)
-    f.kll = K * K;
-    f.kd = 1.0;
-    f.khh = 1.0 / (K * K);
-    return f;
-}
-
-int32_t launch_itail_levels(const dwt2_plan *p, const ITailLevelIO *lv, int n, int count, const ITailFilter &f,
-                            cudaStream_t stream)
-{
-    if (n < 1 || n > MAX_TAIL || (f.radius != 2 && f.radius != 4)) return fail(DWT2_EINVAL);
-    ITailArgs ta;
-    memset(&ta, 0, sizeof(ta));
-    ta.nlev = n;
-    ta.count = count;
-    long long most = 0;
-    for (int k = 0; k < n; ++k) {
-        ta.lv[k] = lv[k];
-        most = std::max<long long>(most, (long long)((lv[k].W + 1) / 2) * ((lv[k].H + 1) / 2) * count);
-    }
-    memcpy(ta.s0, f.s0, sizeof(ta.s0));
-    memcpy(ta.s1, f.s1, sizeof(ta.s1));
-    ta.kll = f.kll;
-    ta.kd = f.kd;
-    ta.khh = f.khh;
-    ta.bar = p->counters + 2 * QUEUE_TAIL;
-    const int resident = f.radius == 2 ? itail_resident<2>() : itail_resident<4>();
-    static const int per_sm_knob = tuning_int("DWT2_TAIL_CTAS", 2, 1, 8);
-    const int per_sm = std::min(resident, per_sm_knob);
-    const long long want = (most + TAIL_THREADS - 1) / TAIL_THREADS;
-    const int grid = int(std::max<long long>(1, std::min<long long>((long long)p->sms * per_sm, want)));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(TAIL_THREADS);
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = f.radius == 2 ? cudaLaunchKernelEx(&cfg, dwt_itail_kernel<2>, ta)
-                                        : cudaLaunchKernelEx(&cfg, dwt_itail_kernel<4>, ta);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return fail(DWT2_ECUDA);
-    }
-    return DWT2_OK;
-}
-
-// last level (counting down from the coarsest) of an inverse that still runs in
-// the inverse tail launch: levels [t, levels) have <= max_quads quads each
-int itail_end(const dwt2_plan *p, int count, long long max_quads)
-{
-    int t = p->levels;
-    while (t - 1 >= 0 && p->levels - (t - 1) <= MAX_TAIL &&
-           (long long)p->geom[t - 1].Wq * p->geom[t - 1].Hq * count <= max_quads)
-        --t;
-    return t;
 }
 
 }  // namespace dwt2_detail
