@@ -105,3 +105,24 @@ def test_gate_positions_cover_every_border_and_strip_edges():
     assert n.min() >= 10 and n.max() < 20
     for row in (10, 11, 18, 19):
         assert set(range(W // 2)) <= set(m[(b == 3) & (n == row)])
+
+
+@pytest.mark.parametrize("wavelet,L", [("cdf53", 3), ("cdf97", 2)])
+def test_gate_inverse_against_oracle(oracle_mod, wavelet, L):
+    """Inverse gate: the timed output is compared with the oracle's inverse of
+    the timed pyramid (bit-exact for 5/3, 1e-4 for 9/7); the round trip is a
+    separate, looser sanity bound."""
+    cfg = workloads.Config("t", L, (workloads.ImageGroup(130, 97, 1, "smooth", 3),), "test")
+    img = cfg.groups[0].image(0)
+    pyr = oracle_mod.forward(img.astype(np.float64), L, round_f32=True, wavelet=wavelet).astype(np.float32)
+    rec = oracle_mod.inverse(pyr.astype(np.float64), L, round_f32=(wavelet == "cdf53"),
+                             wavelet=wavelet).astype(np.float32)
+    r = _fake_single_runner(cfg, rec, img)
+    r.x = torch.from_numpy(pyr)
+    res = bench.gate(r, cfg, _args(wavelet=wavelet, op="inverse"))
+    assert res["status"] == "pass", res
+    bad = rec.copy()
+    bad[50, 60] += 1e-3
+    r = _fake_single_runner(cfg, bad, img)
+    r.x = torch.from_numpy(pyr)
+    assert bench.gate(r, cfg, _args(wavelet=wavelet, op="inverse"))["status"] == "fail"
