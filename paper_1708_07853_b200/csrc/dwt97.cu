@@ -83,7 +83,7 @@ struct K2Args {
     long long ntiles;
     FastDiv fd_img, fd_slabs;              // division by nblk * nslabs and by nslabs (ntiles < 2^31)
     double c0, c1, c2, c3;                 // lifting coefficients (predict, update, predict, update)
-    double sll, sd, shh;                   // output scaling: LL, HL / LH, HH
+    double sll, sd, shh;                   // output scaling: LL, HL / LH (always 1, not applied), HH
     unsigned int *counter;                 // tile queue (queue.cuh)
     int nwarps;
 };
@@ -302,8 +302,8 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
 #pragma unroll
             for (int i = 0; i < QK; ++i) {
                 oLL[i] = (float)(A2[i] * a.sll);
-                oHL[i] = (float)(B2[i] * a.sd);
-                oLH[i] = (float)(C2[i] * a.sd);
+                oHL[i] = (float)B2[i];          // HL, LH scaling: K / K = 1 (DESIGN.md C-B2)
+                oLH[i] = (float)C2[i];
                 oHH[i] = (float)(hh2[i] * a.shh);
             }
             const bool has_odd = n < Hh;
