@@ -132,11 +132,15 @@ template <bool TMA> struct Lay {
     static constexpr int RP = TMA ? BOXW : BOXW + 4;
     static constexpr int SUB = (BOXH * RP + 31) / 32 * 32;       // one box; TMA dst is 128-B aligned
 };
-template <bool TMA> struct Ring {
+template <bool TMA, int NS = S> struct Ring {
     static constexpr int STAGE = NBOX * Lay<TMA>::SUB;          // floats per stage
-    static constexpr int FLOATS = S * STAGE;                    // floats per warp ring
-    static constexpr size_t SMEM = size_t(WARPS) * FLOATS * sizeof(float) + size_t(WARPS) * S * 8;
+    static constexpr int FLOATS = NS * STAGE;                   // floats per warp ring
+    static constexpr size_t SMEM = size_t(WARPS) * FLOATS * sizeof(float) + size_t(WARPS) * NS * 8;
 };
+// Large levels run a 3-stage ring (3 CTAs per SM by shared memory): measured
+// 16384^2 805.5 -> 811.7 Gpix/s (0.982 -> 0.990 of copy); mid-size levels keep
+// 2 stages and 4 CTAs per SM (3 stages there: config 2 616 -> 589, config 4 474 -> 463)
+constexpr int S_LARGE = 3;
 
 static_assert((Ring<true>::STAGE * 4) % 128 == 0 && (Ring<false>::STAGE * 4) % 128 == 0,
               "every ring slot must be 128-byte aligned for TMA");
@@ -218,10 +222,10 @@ __device__ __forceinline__ int grp_row(int off)
     const int k = off & (GG - 1);
     return (k < rem ? k * ca : rem * ca + (k - rem) * cb) + (off / GG) * BOXWG;
 }
-template <bool TMA, int GG> struct RingG {
+template <bool TMA, int GG, int NS = S> struct RingG {
     static constexpr int STAGE = GG > 1 ? SUBG : Ring<TMA>::STAGE;
-    static constexpr int FLOATS = S * STAGE;
-    static constexpr size_t SMEM = size_t(WARPS) * FLOATS * sizeof(float) + size_t(WARPS) * S * 8;
+    static constexpr int FLOATS = NS * STAGE;
+    static constexpr size_t SMEM = size_t(WARPS) * FLOATS * sizeof(float) + size_t(WARPS) * NS * 8;
 };
 static_assert((SUBG * 4) % 128 == 0, "GRP stage slots must stay 128-byte aligned");
 
@@ -728,20 +732,20 @@ __device__ __forceinline__ void storeq(float *p, const float (&x)[QPL], int n, b
 // streams tiles from the work queue through its own TMA ring (producer and
 // consumer in one warp, prefetching across tile boundaries).
 // ---------------------------------------------------------------------------
-template <bool TMA, bool VEC, int AR, int GG>
-__global__ void __launch_bounds__(THREADS, DWT2_MINB)
+template <bool TMA, bool VEC, int AR, int GG, int NS = S>
+__global__ void __launch_bounds__(THREADS, NS == 2 ? DWT2_MINB : 3)
 dwt53_level_kernel(const __grid_constant__ LevelArgs a)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr bool GRP = GG > 1;            // row-grouped TMA, G = GG rows per group
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    float *ring = reinterpret_cast<float *>(smem_raw) + size_t(warp) * RingG<TMA, GG>::FLOATS;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + size_t(WARPS) * RingG<TMA, GG>::FLOATS * sizeof(float)) +
-                     warp * S;
+    float *ring = reinterpret_cast<float *>(smem_raw) + size_t(warp) * RingG<TMA, GG, NS>::FLOATS;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + size_t(WARPS) * RingG<TMA, GG, NS>::FLOATS * sizeof(float)) +
+                     warp * NS;
 
     if (lane == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1u);     // one arrive.expect_tx per stage
+        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1u);     // one arrive.expect_tx per stage
         fence_mbar_init();
     }
     __syncwarp();
@@ -785,11 +789,11 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
         pt_nst = tile_stages(pt);
     }
     // tile ids handed from producer to consumer, in order (warp-private smem
-    // would do too; S + 1 entries suffice because the producer is at most S
-    // stages -- hence at most S tiles -- ahead)
-    int tq[S + 1];
+    // would do too; NS + 1 entries suffice because the producer is at most NS
+    // stages -- hence at most NS tiles -- ahead)
+    int tq[NS + 1];
 #pragma unroll
-    for (int i = 0; i <= S; ++i) tq[i] = -1;
+    for (int i = 0; i <= NS; ++i) tq[i] = -1;
     int tq_head = 0, tq_tail = 0;      // consumer pops at head, producer pushes at tail
     if (pt_id >= 0) {
         tq[0] = pt_id;
@@ -807,12 +811,12 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
             pt_nst = tile_stages(pt);
             pt_j = 0;
 #pragma unroll
-            for (int i = 0; i <= S; ++i)
-                if (i == tq_tail % (S + 1)) tq[i] = pt_id;
+            for (int i = 0; i <= NS; ++i)
+                if (i == tq_tail % (NS + 1)) tq[i] = pt_id;
             ++tq_tail;
         }
-        const int slot = int(prod_seq % S);
-        float *dst = ring + slot * RingG<TMA, GG>::STAGE;
+        const int slot = int(prod_seq % NS);
+        float *dst = ring + slot * RingG<TMA, GG, NS>::STAGE;
         const int r0 = tile_row0(pt) + pt_j * ROWS;
         if (GRP) {
             // G boxes per column box, one per row class (see grp_row).  Rows
@@ -834,7 +838,7 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
                 }
             }
             if (!DWT2_GRP_NOFIX && fr0 + BOXH > a.grp_rows && fr0 < a.flat_rows) {
-                mbar_wait(&bars[slot], (prod_seq / S) & 1u);
+                mbar_wait(&bars[slot], (prod_seq / NS) & 1u);
                 for (int off = 0; off < BOXH; ++off) {
                     const long long fr = fr0 + off;
                     if (fr < a.grp_rows || fr >= a.flat_rows) continue;
@@ -923,14 +927,14 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
     };
 
     // prologue: fill the ring
-    for (int i = 0; i < S; ++i) issue_next();
+    for (int i = 0; i < NS; ++i) issue_next();
 
     // ---- consumer: tiles in the order the producer fetched them
     while (tq_head < tq_tail) {
         int t_id = -1;
 #pragma unroll
-        for (int i = 0; i <= S; ++i)
-            if (i == tq_head % (S + 1)) t_id = tq[i];
+        for (int i = 0; i <= NS; ++i)
+            if (i == tq_head % (NS + 1)) t_id = tq[i];
         ++tq_head;
         const Tile T = decode_tile(a, t_id);
         const int x0 = T.x0;
@@ -963,11 +967,11 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
         RowD E;
         for (int j = 0; j < nst; ++j) {
             const uint32_t k = cons_seq++;
-            const float *slot = ring + int(k % S) * RingG<TMA, GG>::STAGE;
+            const float *slot = ring + int(k % NS) * RingG<TMA, GG, NS>::STAGE;
 #ifdef DWT2_PROF
             const long long tw = clock64();
 #endif
-            mbar_wait(&bars[k % S], (k / S) & 1u);
+            mbar_wait(&bars[k % NS], (k / NS) & 1u);
 #ifdef DWT2_PROF
             t_wait += clock64() - tw;
 #endif
@@ -1082,6 +1086,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode()
 }
 
 typedef void (*KernelFn)(LevelArgs);
+
+// the 3-stage product kernel of large levels (3-D TMA loader, grouped arithmetic)
+KernelFn kernel_large(bool vec)
+{
+    return vec ? dwt53_level_kernel<true, true, AR_GROUPED, 1, S_LARGE> : dwt53_level_kernel<true, false, AR_GROUPED, 1, S_LARGE>;
+}
 
 template <int AR>
 KernelFn kernel_for_ar(bool tma, bool vec)
@@ -1248,7 +1258,10 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     const long long warps_full = (long long)max_ctas * WARPS;
     const TilePolicy &pol = tile_policy();
     long long tb = slab_rows / ((long long)pol.tpw * warps_full);
-    if (pol.tb_large > 0 && slab_rows >= (long long)pol.large_tpw * pol.tb_large * warps_full) {
+    const bool large = pol.tb_large > 0 && slab_rows >= (long long)pol.large_tpw * pol.tb_large * warps_full;
+    static const int use_s3 = tuning_int("DWT2_LARGE_S3", 1, 0, 1);
+    const bool s3 = use_s3 && large && tma && ar == AR_GROUPED;      // the 3-stage kernel (S_LARGE)
+    if (large) {
         // large levels (>= large_tpw tiles per warp at tb_large quad rows):
         // tb_large, measured best from 16384 x 6144 up -- 16384 x 8192 (a
         // config-3 strip at G = 2): 0.82 -> 0.96 of copy against 11-row
@@ -1300,7 +1313,7 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     a.fd_slabs = make_fastdiv(unsigned(a.nslabs));
     a.fd_img = make_fastdiv(unsigned(a.nblk * a.nslabs));
     const long long want_ctas = (ntiles + WARPS - 1) / WARPS;
-    const int grid = int(std::max<long long>(1, std::min<long long>(max_ctas, want_ctas)));
+    const int grid = int(std::max<long long>(1, std::min<long long>(s3 ? p->max_ctas[2] : max_ctas, want_ctas)));
     a.nwarps = grid * WARPS;
     a.static_tiles = ntiles <= a.nwarps ? 1 : 0;
     // the first stage of a tile on the unrolled path: measured faster on
@@ -1316,14 +1329,14 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = grp ? RingG<true, 2>::SMEM : tma ? Ring<true>::SMEM : Ring<false>::SMEM;
+    cfg.dynamicSmemBytes = grp ? RingG<true, 2>::SMEM : s3 ? Ring<true, S_LARGE>::SMEM : tma ? Ring<true>::SMEM : Ring<false>::SMEM;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel_for(tma || grp, vec, ar, grp ? 1 << glog : 1), a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, s3 ? kernel_large(vec) : kernel_for(tma || grp, vec, ar, grp ? 1 << glog : 1), a);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(DWT2_ECUDA);
@@ -1333,7 +1346,7 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
 
 int32_t configure_kernels(int *max_ctas)
 {
-    static int cached[2] = {0, 0};
+    static int cached[3] = {0, 0, 0};
     static std::once_flag once;
     static int32_t status = DWT2_OK;
     std::call_once(once, [] {
@@ -1376,10 +1389,23 @@ int32_t configure_kernels(int *max_ctas)
             }
             cached[t] = sms * per_sm;
         }
+        for (int v = 0; v < 2; ++v)
+            if (cudaFuncSetAttribute(kernel_large(v == 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(Ring<true, S_LARGE>::SMEM)) != cudaSuccess) {
+                status = DWT2_ECUDA;
+                return;
+            }
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_large(true), THREADS,
+                                                          Ring<true, S_LARGE>::SMEM) != cudaSuccess || per_sm < 1) {
+            status = DWT2_ECUDA;
+            return;
+        }
+        cached[2] = sms * per_sm;
     });
     cudaGetLastError();
     max_ctas[0] = cached[0];
     max_ctas[1] = cached[1];
+    max_ctas[2] = cached[2];
     return status;
 }
 
