@@ -126,3 +126,37 @@ def test_gate_inverse_against_oracle(oracle_mod, wavelet, L):
     r = _fake_single_runner(cfg, bad, img)
     r.x = torch.from_numpy(pyr)
     assert bench.gate(r, cfg, _args(wavelet=wavelet, op="inverse"))["status"] == "fail"
+
+
+@pytest.mark.parametrize("L,G", [(1, 2), (1, 3), (3, 4)])
+def test_gate_strip_rank_outputs(oracle_mod, L, G):
+    """Row-strip mode (bench --gpus N): every rank's strip-local Mallat output,
+    cut from the oracle's global pyramid, passes the per-rank gate (level-1
+    coefficients of its own quad rows, incl. its first / last two), and one
+    ulp moved in a strip's edge quad row fails it."""
+    from paper_1708_07853_b200 import distributed as D
+    W, H = 200, 96
+    cfg = workloads.Config("t", L, (workloads.ImageGroup(W, H, 1, "uniform", 4),), "test")
+    img = cfg.groups[0].image(0)
+    full = oracle_mod.forward(img.astype(np.float64), L, round_f32=True).astype(np.float32)
+    lvl1 = oracle_mod.forward(img.astype(np.float64), 1, round_f32=True).astype(np.float32)
+    Wq, Hq, Hh = (W + 1) // 2, (H + 1) // 2, H // 2
+    for g in range(G):
+        r0, r1 = D.strip_rows_levels(H, g, G, L)
+        qs, qe = r0 // 2, (r1 + 1) // 2
+        hq_loc = qe - qs
+        out = np.zeros((r1 - r0, W), np.float32)
+        out[:hq_loc, Wq:] = full[qs:qe, Wq:]                        # HL
+        if L == 1:
+            out[:hq_loc, :Wq] = full[qs:qe, :Wq]                    # LL
+        h0, h1 = min(qs, Hh), min(qe, Hh)
+        out[hq_loc:hq_loc + (h1 - h0), :] = full[Hq + h0:Hq + h1, :]   # LH | HH
+        np.testing.assert_array_equal(out[:hq_loc, Wq:], lvl1[qs:qe, Wq:])
+        r = types.SimpleNamespace(torch=torch, mode="strip", out=torch.from_numpy(out), host_img=img,
+                                  ex=types.SimpleNamespace(r0=r0, r1=r1))
+        res = bench.gate(r, cfg, _args())
+        assert res["status"] == "pass", (g, res)
+        bad = out.copy()
+        bad[hq_loc - 1, Wq + 3] = np.nextafter(bad[hq_loc - 1, Wq + 3], np.float32(np.inf))   # HL, last own row
+        r.out = torch.from_numpy(bad)
+        assert bench.gate(r, cfg, _args())["status"] == "fail", g
