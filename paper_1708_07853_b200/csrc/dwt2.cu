@@ -1288,8 +1288,9 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     // per warp from the queue, so warps on slower SMs (a 1.5x spread of SM
     // throughput under full HBM load) do not set the kernel's length, while
     // most rows still pay the carry-in row of a large tile only.
+    static const int guided_max_tpw = tuning_int("DWT2_GUIDED_MAXTPW", 8, 1, 1024);
     if (pol.guided && io.count == 1 && lenB == 0 && slab_rows >= 16LL * warps_full &&
-        slab_rows / ((long long)a.tb * warps_full) < 8) {
+        slab_rows / ((long long)a.tb * warps_full) < guided_max_tpw) {
         const long long nblk_a = std::max<long long>(1, warps_full / a.nslabs);
         long long tb_a = (pol.guided_a * lenA / 100) / nblk_a;
         tb_a = (tb_a + 1) / PAIRS * PAIRS - 1;                       // tb + 1 whole stages, rounded down
