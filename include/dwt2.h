@@ -175,14 +175,17 @@ int32_t dwt2_forward_strip_level(const dwt2_plan *plan, int32_t level, const flo
  * tensor maps (2 or 4 rows per tensor row) otherwise; an `in` that is only
  * 4-byte aligned, or batched images with gaps between them, take a 1-D
  * bulk-copy loader; an even ceil(W/2) with 8-byte-aligned subband rows gets
- * vector stores.
+ * vector stores.  Launches: one per level, except that the small last levels
+ * (at most 16384 quads each over all images for CDF 5/3, 65536 for the K = 2
+ * wavelets) run together in ONE tail launch (dwt2_plan_info reports the
+ * count).
  * Returns DWT2_OK, DWT2_EINVAL or DWT2_ECUDA. */
 int32_t dwt2_forward(const dwt2_plan *plan, const float *in, float *out, dwt2_stream_t stream);
 
 /* Forward transform of `count` images of the plan's size (count <= the
  * plan's max_count).  Image i is read at in + i * in_stride and written at
  * out + i * out_stride (element strides, >= W * H).  One launch per level
- * covers all images. */
+ * (or the tail launch, see dwt2_forward) covers all images. */
 int32_t dwt2_forward_batched(const dwt2_plan *plan, const float *in, float *out, int32_t count,
                              int64_t in_stride, int64_t out_stride, dwt2_stream_t stream);
 
