@@ -88,6 +88,17 @@ struct K2Args {
     int nwarps;
 };
 
+__device__ __forceinline__ int wssi(int k, int n);
+
+// The same reflection without the integer division when one mirror suffices
+// (|overhang| < n - 1: every index of a slab or window of a level that is
+// not tiny); the edge slabs of the K = 2 kernels call it once per pixel.
+__device__ __forceinline__ int wssi_fast(int k, int n)
+{
+    const int r = k < 0 ? -k : (k >= n ? 2 * (n - 1) - k : k);
+    return (r >= 0 && r < n) ? r : wssi(k, n);
+}
+
 __device__ __forceinline__ int wssi(int k, int n)
 {
     // whole-sample symmetric reflection, any k (period 2 (n - 1))
@@ -126,7 +137,7 @@ __device__ __forceinline__ RawRow load_raw_row(const K2Args &a, const float *img
     } else {
 #pragma unroll
         for (int j = 0; j < 2 * QK; ++j) {
-            const int x = EDGE ? wssi(xb + j, a.W) : xb + j;
+            const int x = EDGE ? wssi_fast(xb + j, a.W) : xb + j;
             R.e[j] = __ldg(p0 + x);
             R.o[j] = __ldg(p1 + x);
         }
@@ -164,6 +175,9 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
     // interior slabs with 16-byte rows: raw rows stream into a per-warp
     // shared-memory ring by cp.async (DS rows in flight, no registers held);
     // edge slabs (horizontal mirroring) load through registers
+    // (measured: edge slabs through the ring too -- lanes outside the image
+    // copying their pixels one by one from the mirrored columns -- are slower
+    // than the register path: 8192^2 112.6 vs 105.8 us)
     constexpr bool ASYNC = VEC && !EDGE;
     constexpr int D = ASYNC ? DS : DR;
     const int Wq = (a.W + 1) >> 1, Wh = a.W >> 1, Hh = a.H >> 1;
@@ -181,12 +195,14 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
                 y0 = wssi(y0, a.H);
                 y1 = wssi(y1, a.H);
             }
-            const float *s0 = in + (long long)y0 * a.in_pitch + xb;
-            const float *s1 = in + (long long)y1 * a.in_pitch + xb;
+            const float *r0 = in + (long long)y0 * a.in_pitch;
+            const float *r1 = in + (long long)y1 * a.in_pitch;
+            float *d0 = wring + (2 * j) * RW + 2 * QK * lane;
+            float *d1 = wring + (2 * j + 1) * RW + 2 * QK * lane;
 #pragma unroll
             for (int q = 0; q < QK / 2; ++q) {
-                cp_async16(wring + (2 * j) * RW + 2 * QK * lane + 4 * q, s0 + 4 * q);
-                cp_async16(wring + (2 * j + 1) * RW + 2 * QK * lane + 4 * q, s1 + 4 * q);
+                cp_async16(d0 + 4 * q, r0 + xb + 4 * q);
+                cp_async16(d1 + 4 * q, r1 + xb + 4 * q);
             }
         } else {
             reg[ASYNC ? 0 : j] = load_raw_row<VEC, EDGE>(a, in, r, xb);
@@ -520,7 +536,7 @@ struct InvCarry {
     k2r hh1, lh1, a, hl1p, lh1p;         // row n-2: HH1, LH1, a, HL'1, LH'1
 };
 
-__device__ __forceinline__ int mqi(int q, int par, int n) { return (wssi(2 * q + par, n) - par) >> 1; }
+__device__ __forceinline__ int mqi(int q, int par, int n) { return (wssi_fast(2 * q + par, n) - par) >> 1; }
 
 struct InvRaw {
     float LL[2], HL[2], LH[2], HH[2];
