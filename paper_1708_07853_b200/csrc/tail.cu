@@ -74,6 +74,13 @@ __device__ __forceinline__ int wss_any(int k, int n)
     return k >= n ? p - k : k;
 }
 
+// one reflection when it suffices (|overhang| < n - 1), else the general form
+__device__ __forceinline__ int wss_fast(int k, int n)
+{
+    const int r = k < 0 ? -k : (k >= n ? 2 * (n - 1) - k : k);
+    return (r >= 0 && r < n) ? r : wss_any(k, n);
+}
+
 // reflection for k in [-2, n + 1], n >= 2 (radius-2 path)
 __device__ __forceinline__ int wss2(int k, int n)
 {
@@ -103,11 +110,11 @@ __global__ void __launch_bounds__(TAIL_THREADS) dwt_tail_kernel(const __grid_con
             const float *x = L.in + img * L.in_img;
             int cx[NT];
 #pragma unroll
-            for (int i = 0; i < NT; ++i) cx[i] = R == 2 ? wss2(2 * m - R + i, W) : wss_any(2 * m - R + i, W);
+            for (int i = 0; i < NT; ++i) cx[i] = R == 2 ? wss2(2 * m - R + i, W) : wss_fast(2 * m - R + i, W);
             double lo[NT], hi[NT];     // row passes: h at column 2m, g at column 2m + 1
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
-                const int y = R == 2 ? wss2(2 * n - R + j, H) : wss_any(2 * n - R + j, H);
+                const int y = R == 2 ? wss2(2 * n - R + j, H) : wss_fast(2 * n - R + j, H);
                 const float *row = x + (long long)y * L.in_pitch;
                 double v[NT];
 #pragma unroll
