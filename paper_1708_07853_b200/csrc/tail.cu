@@ -268,11 +268,16 @@ int32_t launch_tail_levels(const dwt2_plan *p, const TailLevelIO *lv, int n, int
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(TAIL_THREADS);
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    // cooperative: the grid barrier needs every CTA resident at once, which a
+    // cooperative launch guarantees (or refuses) even next to other streams' work
+    static const int coop = tuning_int("DWT2_TAIL_COOP", 1, 0, 1);
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = coop ? 2 : 1;
     const cudaError_t e = f.radius == 2 ? cudaLaunchKernelEx(&cfg, dwt_tail_kernel<2>, ta)
                                         : cudaLaunchKernelEx(&cfg, dwt_tail_kernel<4>, ta);
     if (e != cudaSuccess) {
