@@ -1946,13 +1946,18 @@ int32_t dwt2_forward_host(const dwt2_plan *p, const float *host_in, float *host_
                     cudaMemcpyAsync(host_out + (long long)(g.Hq + h0) * p->W, p->d_out + (long long)(g.Hq + h0) * p->W,
                                     rowb * (h1 - h0), cudaMemcpyDeviceToHost, p->s_d2h);
             } else {
-                // level-1 LH|HH rows are final at once; the top half waits for the coarser levels
+                // level-1 LH|HH rows and the HL part of the LL|HL rows are final
+                // at once; only the LL quadrant waits for the coarser levels
+                cudaStreamWaitEvent(p->s_d2h, ev_k[b], 0);
+                const size_t hlb = size_t(p->W - g.Wq) * sizeof(float);
+                if (hlb > 0)
+                    cudaMemcpy2DAsync(host_out + (long long)q_done * p->W + g.Wq, rowb,
+                                      p->d_out + (long long)q_done * p->W + g.Wq, rowb, hlb, qe - q_done,
+                                      cudaMemcpyDeviceToHost, p->s_d2h);
                 const int h0 = std::min(q_done, p->H / 2), h1 = std::min(qe, p->H / 2);
-                if (h1 > h0) {
-                    cudaStreamWaitEvent(p->s_d2h, ev_k[b], 0);
+                if (h1 > h0)
                     cudaMemcpyAsync(host_out + (long long)(g.Hq + h0) * p->W, p->d_out + (long long)(g.Hq + h0) * p->W,
                                     rowb * (h1 - h0), cudaMemcpyDeviceToHost, p->s_d2h);
-                }
             }
             q_done = qe;
         }
@@ -1962,7 +1967,9 @@ int32_t dwt2_forward_host(const dwt2_plan *p, const float *host_in, float *host_
         if (r != DWT2_OK) return r;
         cudaEventRecord(ev_done[1], s);
         cudaStreamWaitEvent(p->s_d2h, ev_done[1], 0);
-        cudaMemcpyAsync(host_out, p->d_out, rowb * g.Hq, cudaMemcpyDeviceToHost, p->s_d2h);
+        // the level-1 LL quadrant, now the Mallat pyramid of the coarser levels
+        cudaMemcpy2DAsync(host_out, rowb, p->d_out, rowb, size_t(g.Wq) * sizeof(float), g.Hq,
+                          cudaMemcpyDeviceToHost, p->s_d2h);
     }
     cudaEventRecord(ev_done[2], p->s_d2h);
     cudaStreamWaitEvent(s, ev_done[2], 0);

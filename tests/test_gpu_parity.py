@@ -232,7 +232,7 @@ def test_config3_strips_g8_bit_identical():
 # --------------------------------------------------------------------------
 
 def test_host_entry_equals_device():
-    for W, H, L in [(4096, 2048, 1), (1030, 777, 3)]:
+    for W, H, L in [(4096, 2048, 1), (1030, 777, 3), (8192, 8192, 8), (8193, 4099, 5), (5, 2000, 2)]:
         x = workloads.uniform_real(W, H, 9)
         ref = gpu_forward(x, L)
         plan = dwt2.Plan(W, H, L)
