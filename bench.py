@@ -420,18 +420,33 @@ class OursRunner:
             e1.synchronize()
             self.h2d, self.d2h = hin.numel() * 4, hout.numel() * 4
             return e0.elapsed_time(e1) / 1e3 / steps
-        # batch: per group H2D -> batched forward -> D2H
+        # batch: chunks of images pipelined through three streams -- H2D of
+        # chunk i+1 || the batched call on chunk i || D2H of chunk i-1
         hosts = [(torch.empty(x.shape, dtype=torch.float32).pin_memory(),
                   torch.empty(x.shape, dtype=torch.float32).pin_memory()) for _, x, _ in self.items]
         for (hi, _), (_, x, _) in zip(hosts, self.items):
             hi.copy_(x.cpu())
         s = torch.cuda.current_stream()
+        up, down = torch.cuda.Stream(), torch.cuda.Stream()
+        CH = 8                                   # images per chunk
 
         def one():
+            up.wait_stream(s)                    # the previous step's calls are done with the inputs
             for (hi, ho), (plan, x, o) in zip(hosts, self.items):
-                x.copy_(hi, non_blocking=True)
-                self.call(plan, x, o)
-                ho.copy_(o, non_blocking=True)
+                for i0 in range(0, x.shape[0], CH):
+                    i1 = min(x.shape[0], i0 + CH)
+                    with torch.cuda.stream(up):
+                        x[i0:i1].copy_(hi[i0:i1], non_blocking=True)
+                        landed = torch.cuda.Event()
+                        landed.record(up)
+                    s.wait_event(landed)
+                    self.call(plan, x[i0:i1], o[i0:i1])
+                    done = torch.cuda.Event()
+                    done.record(s)
+                    with torch.cuda.stream(down):
+                        down.wait_event(done)
+                        ho[i0:i1].copy_(o[i0:i1], non_blocking=True)
+            s.wait_stream(down)                  # the step ends when its results are on the host
         for _ in range(warm):
             one()
         torch.cuda.synchronize()
