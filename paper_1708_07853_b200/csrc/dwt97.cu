@@ -86,9 +86,41 @@ struct K2Args {
     double sll, sd, shh;                   // output scaling: LL, HL / LH (always 1, not applied), HH
     unsigned int *counter;                 // tile queue (queue.cuh)
     int nwarps;
+    int slab_r, nedge;                     // edge-first order: edge slabs {0} u [slab_r, nslabs), nedge of them
+                                           // per row (0: plain row-block-major order)
 };
 
 __device__ __forceinline__ int wssi(int k, int n);
+
+// Queue index -> (image, row block, slab).  Edge-first order (nedge > 0): the
+// tiles of the edge slabs of every row block come first -- they read through
+// registers with mirrored indices and take longer, so they must not be the
+// tail of the level -- then the interior tiles, row-block-major.
+__device__ __forceinline__ void k2_decode(const K2Args &a, int t, int &img, int &blk, int &slab)
+{
+    if (a.nedge > 0) {
+        const int ne = a.nedge, ni = a.nslabs - a.nedge;
+        const int edge_tiles = a.count * a.nblk * ne;
+        if (t < edge_tiles) {
+            img = t / (a.nblk * ne);
+            const int r = t - img * a.nblk * ne;
+            blk = r / ne;
+            const int e = r - blk * ne;
+            slab = e == 0 ? 0 : a.slab_r + e - 1;
+        } else {
+            const int u = t - edge_tiles;
+            img = u / (a.nblk * ni);
+            const int r = u - img * a.nblk * ni;
+            blk = r / ni;
+            slab = 1 + (r - blk * ni);
+        }
+        return;
+    }
+    img = fdiv(t, a.fd_img);
+    const int rr = t - img * a.nblk * a.nslabs;
+    blk = fdiv(rr, a.fd_slabs);
+    slab = rr - blk * a.nslabs;
+}
 
 // The same reflection without the integer division when one mirror suffices
 // (|overhang| < n - 1: every index of a slab or window of a level that is
@@ -394,13 +426,10 @@ __global__ void __launch_bounds__(KT, DWT2_K2_MINB) dwt_k2_level_kernel(const __
     const int lane = threadIdx.x & 31;
     float *wring = k2_smem + (threadIdx.x >> 5) * (DS * 2 * RW);
     const int Wq = (a.W + 1) >> 1, Hq = (a.H + 1) >> 1;
-    const long long per_img = (long long)a.nblk * a.nslabs;
     for (long long t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane); t < a.ntiles;
          t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane)) {
-        const int img = fdiv(int(t), a.fd_img);
-        const int rr = int(t - img * per_img);
-        const int blk = fdiv(rr, a.fd_slabs);
-        const int slab = rr - blk * a.nslabs;
+        int img, blk, slab;
+        k2_decode(a, int(t), img, blk, slab);
         const int m0 = slab * OUTQ;
         const int n0 = blk * a.tb, n1 = min(n0 + a.tb, Hq);
         // pixel columns 2 (m0 - QK) .. 2 (m0 - QK + SLABQ) - 1 must lie inside the image for the
@@ -468,6 +497,20 @@ int32_t launch_k2_level(const dwt2_plan *p, K2Args a, cudaStream_t s)
     a.ntiles = (long long)a.count * a.nblk * a.nslabs;
     a.fd_img = make_fastdiv(unsigned(a.nblk * a.nslabs));
     a.fd_slabs = make_fastdiv(unsigned(a.nslabs));
+    // edge-first tile order (k2_decode): the edge slabs as the kernel classifies them
+    static const int edge_first = tuning_int("DWT2_K2_EDGEFIRST", 1, 0, 1);
+    a.nedge = 0;
+    if (edge_first && a.nslabs >= 3) {
+        int sr = a.nslabs;
+        while (sr - 1 >= 1) {
+            const int m0 = (sr - 1) * OUTQ;
+            if ((2 * (m0 - QK + SLABQ) > a.W) || (m0 + OUTQ > Wq)) --sr;
+            else break;
+        }
+        a.slab_r = sr;
+        a.nedge = 1 + (a.nslabs - sr);
+        if (a.nedge >= a.nslabs) a.nedge = 0;
+    }
     if (a.ntiles >= (1LL << 31)) return fail(DWT2_EINVAL);
     const long long want = (a.ntiles + KW - 1) / KW;
     const int grid = int(std::max<long long>(1, std::min<long long>(want, warps / KW)));
