@@ -96,7 +96,8 @@ __device__ __forceinline__ int wssi(int k, int n);
 // tiles of the edge slabs of every row block come first -- they read through
 // registers with mirrored indices and take longer, so they must not be the
 // tail of the level -- then the interior tiles, row-block-major.
-__device__ __forceinline__ void k2_decode(const K2Args &a, int t, int &img, int &blk, int &slab)
+template <class Args>
+__device__ __forceinline__ void k2_decode(const Args &a, int t, int &img, int &blk, int &slab)
 {
     if (a.nedge > 0) {
         const int ne = a.nedge, ni = a.nslabs - a.nedge;
@@ -572,6 +573,7 @@ struct K2InvArgs {
     int vec_out;                           // 1: output 16-byte aligned with pitch % 4 == 0 (float4 stores)
     unsigned int *counter;                 // tile queue (queue.cuh)
     int nwarps;
+    int slab_r, nedge;                     // edge-first tile order (k2_decode)
 };
 
 struct InvCarry {
@@ -794,13 +796,10 @@ __global__ void __launch_bounds__(KT, DWT2_K2INV_MINB) dwt_k2_inverse_kernel(con
     const int lane = threadIdx.x & 31;
     float *ring = kinv_smem + (threadIdx.x >> 5) * (IDSK * 4 * 64);
     const int Wq = (a.W + 1) >> 1, Hq = (a.H + 1) >> 1;
-    const long long per_img = (long long)a.nblk * a.nslabs;
     for (long long t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane); t < a.ntiles;
          t = dwt2_queue_fetch(a.counter, a.ntiles, a.nwarps, lane)) {
-        const int img = fdiv(int(t), a.fd_img);
-        const int rr = int(t - img * per_img);
-        const int blk = fdiv(rr, a.fd_slabs);
-        const int slab = rr - blk * a.nslabs;
+        int img, blk, slab;
+        k2_decode(a, int(t), img, blk, slab);
         const int m0 = slab * OUTQ;
         const int n0 = blk * a.tb, n1 = min(n0 + a.tb, Hq);
         // coefficient columns m0 - 2 .. m0 + 61 must exist in every plane for the unmirrored path
@@ -846,6 +845,20 @@ int32_t launch_k2_inverse_level(const dwt2_plan *p, K2InvArgs a, cudaStream_t s)
     a.ntiles = (long long)a.count * a.nblk * a.nslabs;
     a.fd_img = make_fastdiv(unsigned(a.nblk * a.nslabs));
     a.fd_slabs = make_fastdiv(unsigned(a.nslabs));
+    // edge-first tile order (k2_decode): the edge slabs as the kernel classifies them
+    static const int edge_first = tuning_int("DWT2_K2INV_EDGEFIRST", 1, 0, 1);
+    a.nedge = 0;
+    if (edge_first && a.nslabs >= 3) {
+        int sr = a.nslabs;
+        while (sr - 1 >= 1) {
+            const int m0 = (sr - 1) * OUTQ;
+            if ((m0 + 62 > (a.W >> 1)) || (m0 + OUTQ > Wq)) --sr;
+            else break;
+        }
+        a.slab_r = sr;
+        a.nedge = 1 + (a.nslabs - sr);
+        if (a.nedge >= a.nslabs) a.nedge = 0;
+    }
     if (a.ntiles >= (1LL << 31)) return fail(DWT2_EINVAL);
     const long long want = (a.ntiles + KW - 1) / KW;
     const int grid = int(std::max<long long>(1, std::min<long long>(want, warps / KW)));
