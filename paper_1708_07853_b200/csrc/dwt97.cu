@@ -832,10 +832,11 @@ int32_t launch_k2_inverse_level(const dwt2_plan *p, K2InvArgs a, cudaStream_t s)
     long long tb = slab_rows / (tpw * warps);
     static const int min_tb = tuning_int("DWT2_K2INV_MINTB", 16, 4, 512);
     tb = std::max<long long>(min_tb, std::min<long long>(512, tb));
-    // levels with >= 64 quad rows per warp: 20-row tiles (measured: 16384^2
-    // 0.765 -> 0.766, 16384 x 6144 0.64 -> 0.70, 8192^2 0.638 -> 0.644 of copy
-    // against the tpw-derived height; smaller levels keep it)
-    static const int tb_large = tuning_int("DWT2_K2INV_TB", 20, 0, 512);
+    // levels with >= 64 quad rows per warp: 32-row tiles (measured with the
+    // edge-first order: 16384^2 0.821 -> 0.838, 8192^2 0.721 -> 0.729 of copy
+    // against 20-row tiles; 48 rows: 0.855 / 0.685; smaller levels keep the
+    // tpw-derived height)
+    static const int tb_large = tuning_int("DWT2_K2INV_TB", 32, 0, 512);
     if (tb_large > 0 && slab_rows >= 64 * warps) tb = tb_large;
     // small levels: one short tile per warp (as the forward, launch_k2_level)
     static const int small_f = tuning_int("DWT2_K2INV_SMALLF", 1, 0, 64);
