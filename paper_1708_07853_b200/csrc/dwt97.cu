@@ -58,7 +58,14 @@ constexpr int RW = 2 * SLABQ;              // floats per staged pixel row (= 64 
 #define DWT2_K2_DS 5                      // measured: 5 > 4 > 6 > 8 > 2 (the row loop is unrolled DS times: i-cache)
 #endif
 constexpr int DS = DWT2_K2_DS;             // raw quad rows in flight per warp (shared-memory ring, cp.async)
-constexpr int DR = 1;                      // raw quad rows in flight per warp on the register path (edge slabs)
+#ifndef DWT2_K2_DR
+#define DWT2_K2_DR 1
+#endif
+constexpr int DR = DWT2_K2_DR;             // raw quad rows in flight per warp on the register path (edge slabs)
+#ifndef DWT2_K2INV_DR
+#define DWT2_K2INV_DR 2                    // the inverse's register path: 2 rows (measured: config 3 682 -> 697 Gpix/s)
+#endif
+constexpr int IDR = DWT2_K2INV_DR;
 constexpr size_t K2_SMEM = size_t(KW) * DS * 2 * RW * sizeof(float);
 static_assert(QK == 2 || QK == 4, "2 or 4 quads per lane");
 
@@ -627,7 +634,7 @@ constexpr size_t KINV_SMEM = size_t(KW) * IDSK * 4 * 64 * sizeof(float);
 template <bool EDGE, bool ASYNC>
 __device__ void kinv_tile(const K2InvArgs &a, float *ring, int img, int m0, int n0, int n1, int lane)
 {
-    constexpr int D = ASYNC ? IDSK : 1;
+    constexpr int D = ASYNC ? IDSK : IDR;
     InvCarry cy[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) cy[i] = InvCarry{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
