@@ -1,7 +1,7 @@
 # Round-2 round-style run: smoke, the default bench line, the reference arm, every
 # config and every 8f row through bench.py (JSON lines -> gpurun_out/r2bench/)
 set -x
-B=gpurun_out/r2bench
+B=gpurun_out/r2bench_final
 mkdir -p $B
 timeout 300 python __graft_entry__.py smoke
 timeout 900 python bench.py > $B/default_c3.json 2> $B/default_c3.err; tail -c 300 $B/default_c3.json
