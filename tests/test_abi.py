@@ -54,6 +54,14 @@ def test_library_is_sm100a(lib):
     assert "DFMA" in sass             # fp64 register arithmetic
 
 
+def test_product_library_reads_no_environment(lib):
+    """The tile-policy knobs are compiled in only for -DDWT2_TUNING builds
+    (dwt2_internal.h tuning_int): the product library's behaviour and timing
+    cannot depend on the caller's environment."""
+    out = subprocess.run(["nm", "-D", "--undefined-only", dwt2.LIB_PATH], capture_output=True, text=True).stdout
+    assert "getenv" not in out and "secure_getenv" not in out
+
+
 def test_static_strings(lib):
     assert "sm_100a" in dwt2.version()
     assert dwt2.error_string(0) == "ok"
