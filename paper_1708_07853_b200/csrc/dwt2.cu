@@ -189,6 +189,8 @@ struct alignas(64) LevelArgs {
     int glog;                         // GRP: log2 G, G = rows per 16-byte-aligned row group (2 or 4)
     long long grp_rows;               // GRP: flat rows covered by whole groups (G floor(flat_rows / G))
     long long flat_rows;              // GRP: count * in_rows
+    int rev;                          // 1: images and quad rows in reverse order (tile t -> mirrored rows)
+    int rsum;                         // rev: qa0 + the end of the level's quad rows (mirror q -> rsum - q)
 };
 
 // Row-grouped TMA (GRP) for row pitches that are not a multiple of 16 bytes:
@@ -366,6 +368,12 @@ __device__ __forceinline__ Tile decode_tile(const LevelArgs &a, int t)
     } else {
         T.qa = a.qb0 + (blk - a.nblk_a) * a.tb_b;
         T.qb = imin(T.qa + a.tb_b, a.qb1);
+    }
+    if (a.rev) {
+        const int qa = T.qa;
+        T.qa = a.rsum - T.qb;
+        T.qb = a.rsum - qa;
+        T.img = a.count - 1 - T.img;
     }
     return T;
 }
@@ -1326,6 +1334,14 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     static const int env_uf = tuning_int("DWT2_UNROLL_FIRST", -1, 0, 1);
     a.unroll_first = env_uf >= 0 ? env_uf : ((a.tb_b != a.tb || a.qb1 > a.qb0 || grp || a.static_tiles) ? 1 : 0);
     a.counter = p->counters + 2 * ((queue ? QUEUE_STRIP_BOUNDARY : QUEUE_FORWARD) + level);
+    // reverse order on every other level of a pyramid: level k + 1 then starts
+    // on the LL rows level k wrote last, still in L2 (config 4: level 2 reads
+    // 64 -> 53 MB from DRAM, the step 142.8 -> 141.3 us; scripts/r2/gpu_rev.sh)
+    static const int rev_mode = tuning_int("DWT2_REV", 1, 0, 1);
+    if (rev_mode && (level & 1) && (lenB == 0 || qb0 == qa1)) {
+        a.rev = 1;
+        a.rsum = qa0 + (lenB ? qb1 : qa1);
+    }
 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
