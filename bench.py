@@ -8,8 +8,9 @@ every level of the forward transform of the config's image(s) (and, for row
 strips at N > 1, the ghost-row exchange).  Default workload: BASELINE.json
 config 3 (16384 x 16384 fp32, 1 level), the configuration the north-star
 target ("70 % of HBM bandwidth per level on 16384 x 16384 fp32") is stated on;
-at N > 1 it is split into N row strips with an NCCL halo exchange (strong
-scaling: the image is fixed).  Inputs are 1 GiB, larger than the 126 MB L2,
+at N > 1 it is split into N row strips whose halo rows the boundary kernels
+read from the neighbour GPUs' memory (``--exchange peer``; ``nccl``: grouped
+send/recv per level) -- strong scaling: the image is fixed.  Inputs are 1 GiB, larger than the 126 MB L2,
 so no L2 flush is needed between steps.
 
 Timing: W untimed warm-up steps, then exactly K steps bracketed by a barrier
@@ -95,7 +96,11 @@ def parse():
                     help="forward with one of the paper's schemes, one kernel per step (SURVEY 8f N1)")
     ap.add_argument("--wavelet", default="cdf53", choices=["cdf53", "cdf97"],
                     help="cdf97: the K = 2 non-separable kernel (SURVEY 8f N4); single-image and batch configs")
-    ap.add_argument("--no-overlap", action="store_true", help="strips: exchange, then one launch")
+    ap.add_argument("--no-overlap", action="store_true", help="strips, --exchange nccl: exchange, then one launch")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="row strips (N > 1): peer = halo rows read from the neighbours' memory inside the "
+                         "BOUNDARY kernels (CUDA IPC over NVLink; the step is one CUDA graph); nccl = grouped "
+                         "NCCL send/recv of the ghost rows per level, host-launched")
     ap.add_argument("--no-graph", action="store_true", help="launch every step from the host instead of "
                     "replaying a CUDA graph of it")
     ap.add_argument("--no-e2e", action="store_true")
@@ -198,7 +203,8 @@ def describe(cfg, world, steps=20):
             else ("timed steps cycle over %d input/output pairs, each reused only after > 2x L2 of other traffic "
                   "(or read once); L2 flushed (256 MB read pass) once before the timed region"
                   % buffer_pairs(cfg, steps)),
-            "parallelism": ("row strips x%d, NCCL halo exchange per level" % world if cfg.name in ("1", "2", "3", "4", "4b")
+            "parallelism": ("row strips x%d, %s halo exchange per level" % (world, OursRunner.exchange_label())
+                            if cfg.name in ("1", "2", "3", "4", "4b")
                             and world > 1 else ("image shards x%d, no communication" % world if world > 1
                                                 else "single GPU"))}
 
@@ -280,12 +286,17 @@ class OursRunner:
             g = cfg.groups[0]
             img = g.image(0)
             self.sha.update(img.tobytes())
-            self.ex = D.StripPyramid(g.width, g.height, rank, world, cfg.levels, device=device)
+            if self.exchange == "peer":
+                self.ex = D.PeerStripPyramid(g.width, g.height, rank, world, cfg.levels, device=device)
+                self.ex.connect()              # all_gather of the CUDA IPC descriptors (once)
+                self.splan = None
+            else:
+                self.ex = D.StripPyramid(g.width, g.height, rank, world, cfg.levels, device=device)
+                self.splan = dwt2.StripPlan(g.width, g.height, self.ex.r0, self.ex.r1, cfg.levels)
             r0, r1 = self.ex.r0, self.ex.r1
             self.ex.strip.copy_(torch.from_numpy(np.ascontiguousarray(img[r0:r1])))
-            self.splan = dwt2.StripPlan(g.width, g.height, r0, r1, cfg.levels)
             self.out = self.ex.out
-            self.launches = cfg.levels * (1 if self.overlap_off else 2)
+            self.launches = cfg.levels * (1 if (self.overlap_off and self.exchange == "nccl") else 2)
             self.algo_bytes = sum(BYTES_PER_PX * w * (re - rb) for (w, h, rb, re, gt, gb) in self.ex.geom)
             self.level1_bytes = BYTES_PER_PX * g.width * (r1 - r0)
             self.pixels = g.width * (r1 - r0)
@@ -293,7 +304,18 @@ class OursRunner:
             self.host_img = img
 
     overlap_off = False
+    exchange = "peer"
     wavelet = "cdf53"
+
+    @classmethod
+    def exchange_label(cls):
+        return "peer-memory (NVLink loads in the boundary kernels)" if cls.exchange == "peer" else "NCCL send/recv"
+
+    def strip_step(self):
+        if self.exchange == "peer":
+            self.ex.step()
+        else:
+            self.D.strip_pyramid_step(self.ex, self.splan, overlap=not self.overlap_off)
     steps = 20
     op = "forward"
     scheme = "fused"
@@ -323,7 +345,7 @@ class OursRunner:
             for plan, x, out in self.items:
                 self.call(plan, x, out)
         else:
-            self.D.strip_pyramid_step(self.ex, self.splan, overlap=not self.overlap_off)
+            self.strip_step()
 
     def level1_kernel_ms(self, iters):
         """Average duration of the dominant kernel (level 1: 3/4 of the
@@ -407,7 +429,7 @@ class OursRunner:
             s = torch.cuda.current_stream()
             def one():
                 self.ex.strip.copy_(hin, non_blocking=True)
-                self.D.strip_pyramid_step(self.ex, self.splan, overlap=True)
+                self.strip_step()
                 hout.copy_(self.out, non_blocking=True)
             for _ in range(warm):
                 one()
@@ -857,6 +879,7 @@ def main():
         dist.barrier()          # communicator up before the first grouped send/recv (all ranks)
 
     OursRunner.overlap_off = args.no_overlap
+    OursRunner.exchange = args.exchange
     OursRunner.steps = args.steps
     OursRunner.op = args.op
     OursRunner.scheme = args.scheme
@@ -878,7 +901,7 @@ def main():
         runner.step()
     torch.cuda.synchronize()
     graph = None
-    if not args.no_graph and runner.mode != "strip":
+    if not args.no_graph and (runner.mode != "strip" or args.exchange == "peer"):
         # the K timed steps as ONE CUDA graph (the level kernels keep their
         # programmatic dependent-launch edges): no host launch gaps, and the
         # NVML sampler thread cannot gate the GPU

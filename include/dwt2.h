@@ -199,6 +199,108 @@ int32_t dwt2_forward_batched(const dwt2_plan *plan, const float *in, float *out,
 int32_t dwt2_forward_strip(const dwt2_plan *plan, const float *in, float *out, int32_t part,
                            dwt2_stream_t stream);
 
+/* ---- Row strips with the halo exchange fused into the boundary kernels --
+ *
+ * The paper's synchronisation point between cores is the exchange of the
+ * samples a step needs from its neighbours (section 3; the
+ * row bands of SPEC.md L313-318).  A peer strip context replaces the message
+ * exchange of dwt2_forward_strip_level (ghost rows copied by NCCL before the
+ * BOUNDARY launch) with device-side PEER READS: the boundary kernel of level
+ * k waits on the neighbour's level-k ready flag and loads the 2 rows above /
+ * 1 row below straight from the neighbour's buffer (NVLink peer memory
+ * mapped through CUDA IPC, or the same device for ranks emulated in one
+ * process).  No host call sits between the levels, so a whole step is a
+ * stream-ordered sequence of 2 launches per level (CUDA-graph capturable).
+ *
+ * Synchronisation (flags in the context's own device memory, epochs counted
+ * on the device): the INTERIOR launch of level 0 advances the rank's epoch e;
+ * the INTERIOR launch of every level k publishes ready[k] = e once it runs
+ * (the level-k input rows are final: they were written by level k-1, or by
+ * the caller for k = 0); the BOUNDARY launch of level k waits until each
+ * neighbour's ready[k] >= e, then reads its rows.  The last level's BOUNDARY
+ * launch publishes done = e and, in DWT2_PEER_RANKS mode, waits until each
+ * neighbour's done >= e, so when a step has completed on a rank's stream no
+ * neighbour still reads that rank's buffers: the caller may then rewrite the
+ * level-0 rows, and the next step may overwrite every level.  A wait that
+ * exceeds the context's timeout gives up (the step's output is then invalid)
+ * and latches DWT2_ETIMEOUT, reported by dwt2_peer_strip_status. */
+
+enum {
+    DWT2_PEER_RANKS = 0,       /* one rank per GPU (or process), running concurrently */
+    DWT2_PEER_SEQUENTIAL = 1   /* every rank in one process and stream order: for each level, all ranks'
+                                  INTERIOR parts, then all ranks' BOUNDARY parts (1-GPU emulation);
+                                  no end-of-step wait; dwt2_peer_strip_forward is rejected */
+};
+
+enum { DWT2_ETIMEOUT = -5 };   /* a peer flag wait timed out (dwt2_peer_strip_status) */
+
+typedef struct dwt2_peer_strip dwt2_peer_strip;
+
+/* What a neighbour needs to map a context: plain bytes, safe to send through
+ * any host channel (the Python binding uses torch.distributed all_gather). */
+typedef struct {
+    uint8_t ipc_handle[64];    /* cudaIpcMemHandle_t of the context's single device allocation */
+    uint64_t base;             /* that allocation's address in the exporting process */
+    int64_t pid;               /* exporting process: the same process maps `base` directly */
+    int32_t device;            /* CUDA ordinal in the exporting process */
+    int32_t width, global_height, levels;
+    int32_t row_begin, row_end;            /* level-0 strip rows */
+    int32_t timeout_ms;
+    int32_t reserved;
+    int64_t owned_off[32];     /* byte offset (from base) of level k's first owned row */
+    int64_t pitch[32];         /* level k's row pitch, floats */
+    int64_t flags_off;         /* byte offset of the flag block */
+} dwt2_peer_desc_t;
+
+/* Allocates, on the plan's device, every level's ghost-padded input buffer of
+ * the multi-level strip plan `plan` (dwt2_plan_create_strip_levels; row
+ * pitches rounded up to 4 floats) and the flag block, in ONE cudaMalloc
+ * (exportable through CUDA IPC).  The context keeps a pointer to `plan`,
+ * which must outlive it.  timeout_ms bounds every flag wait (<= 0: 10000).
+ * Returns NULL on error (dwt2_last_error()). */
+dwt2_peer_strip *dwt2_peer_strip_create(const dwt2_plan *plan, int32_t timeout_ms);
+
+/* Level k's owned rows in the context: *owned = the first owned row (device),
+ * *pitch in floats.  Level 0's owned rows are where the caller writes the
+ * strip's pixels (row_end - row_begin rows of `width` floats) before a step. */
+int32_t dwt2_peer_strip_buffer(const dwt2_peer_strip *ctx, int32_t level, float **owned, int64_t *pitch);
+
+/* Fills *desc for the neighbours of this rank. */
+int32_t dwt2_peer_strip_export(const dwt2_peer_strip *ctx, dwt2_peer_desc_t *desc);
+
+/* Maps the neighbours: `above` is the rank owning the rows just above
+ * row_begin (NULL iff row_begin == 0), `below` the rank owning the rows from
+ * row_end (NULL iff row_end == global_height).  Their geometry must match
+ * (same width, height, levels; above->row_end == row_begin, below->row_begin
+ * == row_end), else DWT2_EINVAL.  Descriptors of another process are opened
+ * with cudaIpcOpenMemHandle (peer access over NVLink); those of this process
+ * are used directly.  mode: DWT2_PEER_RANKS or DWT2_PEER_SEQUENTIAL.  Call
+ * once, before the first step; DWT2_ECUDA if a mapping fails. */
+int32_t dwt2_peer_strip_connect(dwt2_peer_strip *ctx, const dwt2_peer_desc_t *above,
+                                const dwt2_peer_desc_t *below, int32_t mode);
+
+/* One part of level k of a step: DWT2_STRIP_INTERIOR (the fused level kernel
+ * on the quad rows that read no neighbour row; level 0 also advances the
+ * epoch) or DWT2_STRIP_BOUNDARY (waits for the neighbours, then computes the
+ * first / last quad row from the neighbours' rows in peer memory).  Parts
+ * must be issued in the order INTERIOR(0), BOUNDARY(0), INTERIOR(1), ... on
+ * one stream of each rank.  out: the strip-local Mallat pyramid (W x (row_end
+ * - row_begin), pitch W, device), as dwt2_forward_strip_level writes it. */
+int32_t dwt2_peer_strip_level(dwt2_peer_strip *ctx, int32_t level, int32_t part, float *out,
+                              dwt2_stream_t stream);
+
+/* A whole step (every level, both parts; 2 launches per level, no host
+ * synchronisation).  DWT2_PEER_RANKS mode only. */
+int32_t dwt2_peer_strip_forward(dwt2_peer_strip *ctx, float *out, dwt2_stream_t stream);
+
+/* DWT2_OK, or DWT2_ETIMEOUT once any flag wait of this context has timed out
+ * (reads device memory: synchronises with the device). */
+int32_t dwt2_peer_strip_status(const dwt2_peer_strip *ctx);
+
+/* Unmaps the neighbours and frees the context (no step may be in flight, on
+ * this rank or on a neighbour reading it).  NULL is a no-op. */
+void dwt2_peer_strip_destroy(dwt2_peer_strip *ctx);
+
 /* End-to-end call on HOST buffers: host_in (W x H fp32) is copied to the
  * device, transformed, and the Mallat result copied back to host_out, all on
  * `stream`; returns after the stream has drained (the only synchronising

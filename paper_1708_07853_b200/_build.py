@@ -12,7 +12,7 @@ import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-SRCS = [os.path.join(PKG, "csrc", f) for f in ("dwt2.cu", "inverse.cu", "schemes.cu", "dwt97.cu", "tail.cu")]
+SRCS = [os.path.join(PKG, "csrc", f) for f in ("dwt2.cu", "inverse.cu", "schemes.cu", "dwt97.cu", "tail.cu", "peer.cu")]
 # every source and header under csrc/ (an edit to any of them rebuilds the library)
 DEPS = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")) + glob.glob(os.path.join(PKG, "csrc", "*.h")) +
               glob.glob(os.path.join(PKG, "csrc", "*.cuh")))

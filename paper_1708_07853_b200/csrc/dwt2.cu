@@ -191,6 +191,8 @@ struct alignas(64) LevelArgs {
     long long flat_rows;              // GRP: count * in_rows
     int rev;                          // 1: images and quad rows in reverse order (tile t -> mirrored rows)
     int rsum;                         // rev: qa0 + the end of the level's quad rows (mirror q -> rsum - q)
+    unsigned int *peer_flags;         // peer strip context (peer.cu): publish ready[peer_level] at entry, else null
+    int peer_level;
 };
 
 // Row-grouped TMA (GRP) for row pitches that are not a multiple of 16 bytes:
@@ -770,6 +772,9 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
 #endif
     pdl_launch_dependents();
     pdl_wait();
+    // peer strip step (peer.cu): every earlier level of this rank is complete
+    // here, so this level's input rows are final -- tell the neighbours
+    if (a.peer_flags != nullptr && blockIdx.x == 0 && threadIdx.x == 0) peer_publish_ready(a.peer_flags, a.peer_level);
 #ifdef DWT2_PROF
     if (threadIdx.x == 0 && blockIdx.x < 4096) {
         unsigned smid;
@@ -1135,6 +1140,8 @@ struct LaunchIO {
     long long out_pitch, out_img_stride;
     int out_q0, hq_local;     // strip-local quad row 0, LL rows present in out (LH offset)
     int count;
+    unsigned int *peer_flags; // peer strip INTERIOR launches: the rank's flag block (else null)
+    int peer_level;
 };
 
 // Tile-size policy of the work queue (measured on B200).
@@ -1194,9 +1201,11 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     a.nslabs = (W + SLAB - 1) / SLAB;
     a.count = io.count;
     a.qa0 = qa0; a.qa1 = qa1; a.qb0 = qb0; a.qb1 = qb1;
+    a.peer_flags = io.peer_flags;
+    a.peer_level = io.peer_level;
     const int lenA = qa1 - qa0, lenB = qb1 - qb0;
     const long long slab_rows = (long long)io.count * a.nslabs * (lenA + lenB);
-    if (slab_rows == 0) return DWT2_OK;
+    if (slab_rows == 0) return io.peer_flags ? launch_peer_publish(io.peer_flags, io.peer_level, stream) : DWT2_OK;
 
     const bool tma = !DWT2_FORCE_GENERIC && aligned(io.in, 16) && (io.in_pitch * 4) % 16 == 0 &&
                      (io.count == 1 || (io.in_img_stride * 4) % 16 == 0);
@@ -1805,8 +1814,12 @@ int32_t dwt2_strip_level_info(const dwt2_plan *p, int32_t level, dwt2_strip_leve
     return DWT2_OK;
 }
 
-int32_t dwt2_forward_strip_level(const dwt2_plan *p, int32_t level, const float *in, int64_t in_pitch,
-                                 float *ll_out, int64_t ll_pitch, float *out, int32_t part, dwt2_stream_t stream)
+}  // extern "C"
+
+namespace dwt2_detail {
+
+int32_t strip_level_launch(const dwt2_plan *p, int level, const float *in, long long in_pitch, float *ll_out,
+                           long long ll_pitch, float *out, int part, cudaStream_t stream, unsigned int *peer_flags)
 {
     dwt2_strip_level_t L;
     if (!p || !in || !out || !p->strip || part < 0 || part > 2 || !aligned(in, 4) || !aligned(out, 4) ||
@@ -1850,6 +1863,8 @@ int32_t dwt2_forward_strip_level(const dwt2_plan *p, int32_t level, const float 
         io.ll_pitch = ll_pitch;
     }
     io.ll_img_stride = io.ll_pitch * (qe - qs);
+    io.peer_flags = peer_flags;
+    io.peer_level = level;
     const int ia = qs + (L.ghost_top ? 1 : 0), ib = qe - (L.ghost_bot ? 1 : 0);
     int a0, a1, b0 = 0, b1 = 0;
     if (part == DWT2_STRIP_ALL) {
@@ -1864,11 +1879,22 @@ int32_t dwt2_forward_strip_level(const dwt2_plan *p, int32_t level, const float 
     }
     // BOUNDARY launches use their own work-queue counters, so they may run on
     // another stream concurrently with the INTERIOR launch of the same level
-    int32_t r = launch_level(p, level, L.width, L.global_height, io, a0, a1, b0, b1,
-                             reinterpret_cast<cudaStream_t>(stream), part == DWT2_STRIP_BOUNDARY ? 1 : 0);
+    int32_t r = launch_level(p, level, L.width, L.global_height, io, a0, a1, b0, b1, stream,
+                             part == DWT2_STRIP_BOUNDARY ? 1 : 0);
     if (r != DWT2_OK) return r;
     g_last_error = DWT2_OK;
     return DWT2_OK;
+}
+
+}  // namespace dwt2_detail
+
+extern "C" {
+
+int32_t dwt2_forward_strip_level(const dwt2_plan *p, int32_t level, const float *in, int64_t in_pitch,
+                                 float *ll_out, int64_t ll_pitch, float *out, int32_t part, dwt2_stream_t stream)
+{
+    return strip_level_launch(p, level, in, in_pitch, ll_out, ll_pitch, out, part,
+                              reinterpret_cast<cudaStream_t>(stream), nullptr);
 }
 
 int32_t dwt2_forward_strip(const dwt2_plan *p, const float *in, float *out, int32_t part, dwt2_stream_t stream)
@@ -2055,6 +2081,7 @@ const char *dwt2_error_string(int32_t code)
     case DWT2_ENOMEM: return "out of memory";
     case DWT2_ECUDA: return "CUDA error";
     case DWT2_EUNSUPPORTED: return "unsupported (boundary mode or device)";
+    case DWT2_ETIMEOUT: return "peer flag wait timed out";
     default: return "unknown error";
     }
 }

@@ -129,6 +129,37 @@ struct dwt2_plan {
 
 namespace dwt2_detail {
 
+// ---- peer strip contexts (peer.cu): flag block layout (uint32 words)
+constexpr int PEER_EPOCH = 0;        // the rank's step epoch (advanced by the level-0 INTERIOR launch)
+constexpr int PEER_DONE = 1;         // epoch whose last-level BOUNDARY launch has finished reading the neighbours
+constexpr int PEER_ERR = 2;          // nonzero: a flag wait timed out
+constexpr int PEER_CTR = 3;          // BOUNDARY CTAs finished (last level; self-resetting)
+constexpr int PEER_READY = 8;        // + k: epoch whose level-k input rows are final
+constexpr int PEER_FLAG_WORDS = PEER_READY + MAX_LEVELS;
+
+#ifdef __CUDACC__
+// Publish "level `level` input rows of this rank are final for the current
+// epoch" (one thread, after griddepcontrol.wait: every earlier launch of the
+// rank's step has completed and its writes are visible).  Level 0 advances
+// the epoch.  The system-scope fence makes those writes visible to a peer GPU
+// that acquires the flag over NVLink before it reads the rows.
+__device__ __forceinline__ void peer_publish_ready(unsigned int *f, int level)
+{
+    volatile unsigned int *vf = f;
+    unsigned e = vf[PEER_EPOCH];
+    if (level == 0) vf[PEER_EPOCH] = ++e;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f + PEER_READY + level), "r"(e) : "memory");
+}
+#endif
+
+// a one-thread launch of peer_publish_ready (strips whose INTERIOR part is empty)
+int32_t launch_peer_publish(unsigned int *flags, int level, cudaStream_t stream);
+
+// dwt2_forward_strip_level with an optional peer flag block (peer.cu INTERIOR parts)
+int32_t strip_level_launch(const dwt2_plan *p, int level, const float *in, long long in_pitch, float *ll_out,
+                           long long ll_pitch, float *out, int part, cudaStream_t stream, unsigned int *peer_flags);
+
 // ---- tail kernel (tail.cu): the small last levels of a forward in one launch
 constexpr int MAX_TAIL = 16;
 

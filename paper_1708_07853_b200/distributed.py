@@ -302,3 +302,110 @@ def place_pyramid_output(full: np.ndarray, strip_out: np.ndarray, W: int, H: int
         if h1 > h0:
             full[Hq + h0:Hq + h1, :w] = strip_out[hq_loc:hq_loc + (h1 - h0), :w]   # LH | HH
         w, h, rb, re = Wq, Hq, qs, qe
+
+
+# ---- peer-memory halo (include/dwt2.h "peer strip context") -----------------
+#
+# The same row strips as StripPyramid, with the exchange fused into the level
+# kernels: every rank's level buffers live in one device allocation whose
+# CUDA IPC handle the neighbours map; the BOUNDARY kernel of a level reads the
+# 2 rows above / 1 row below from the neighbour's memory over NVLink once the
+# neighbour's flag says they are final.  Host side, a step is 2 launches per
+# level with no wait, so it can be captured in a CUDA graph.  The descriptors
+# (plain bytes) travel once, through all_gather_object on the process group.
+
+def peer_neighbours(descs: list, rank: int) -> tuple:
+    """(above, below) descriptor bytes of `rank` from the all-gathered list,
+    checked for matching geometry (the C side checks again): the rank above
+    must end where this strip begins, the rank below begin where it ends."""
+    from . import dwt2
+    me = dwt2.PeerDesc.from_bytes(descs[rank])
+    above = below = None
+    if rank > 0:
+        above = dwt2.PeerDesc.from_bytes(descs[rank - 1])
+        if above.row_end != me.row_begin:
+            raise ValueError(f"rank {rank}: the strip above ends at row {above.row_end}, this one begins at "
+                             f"{me.row_begin}")
+    if rank + 1 < len(descs):
+        below = dwt2.PeerDesc.from_bytes(descs[rank + 1])
+        if below.row_begin != me.row_end:
+            raise ValueError(f"rank {rank}: the strip below begins at row {below.row_begin}, this one ends at "
+                             f"{me.row_end}")
+    for d in (above, below):
+        if d is not None and (d.width, d.global_height, d.levels) != (me.width, me.global_height, me.levels):
+            raise ValueError(f"rank {rank}: neighbour geometry {d.width}x{d.global_height} L{d.levels} differs")
+    return above, below
+
+
+def gather_descriptors(desc_bytes: bytes, group=None) -> list:
+    """All ranks' descriptor bytes, in rank order (one all_gather_object)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, desc_bytes, group=group)
+    return out
+
+
+class PeerStripPyramid:
+    """Rank's L-level row strip with peer-memory halos.  Fill ``strip`` (the
+    level-0 owned rows, inside the C context's allocation), then ``step()``;
+    the strip-local Mallat pyramid lands in ``out`` (the layout of
+    StripPyramid.out).  ``connect()`` is collective over the process group.
+    Emulated ranks (several in one process, tests and 1-GPU measurement) use
+    ``connect_local`` and ``sequential_step``."""
+
+    def __init__(self, width: int, height: int, rank: int, world: int, levels: int = 1, device=None,
+                 timeout_ms: int = 0):
+        import torch
+        from . import dwt2
+        self.width, self.height, self.rank, self.world, self.levels = width, height, rank, world, levels
+        self.r0, self.r1 = strip_rows_levels(height, rank, world, levels)
+        self.geom = level_rows(width, height, self.r0, self.r1, levels)
+        self.ghost_top, self.ghost_bot = self.geom[0][4], self.geom[0][5]
+        self.plan = dwt2.StripPlan(width, height, self.r0, self.r1, levels)
+        self.ctx = dwt2.PeerStrip(self.plan, timeout_ms)
+        self.out = torch.empty((self.r1 - self.r0, width), dtype=torch.float32, device=device)
+
+    @property
+    def strip(self):
+        """Level-0 owned rows (write the strip's pixels here before a step)."""
+        return self.ctx.owned(0)
+
+    def owned(self, k: int):
+        return self.ctx.owned(k)
+
+    def export(self) -> bytes:
+        return self.ctx.export().to_bytes()
+
+    def connect(self, group=None):
+        from . import dwt2
+        above, below = peer_neighbours(gather_descriptors(self.export(), group), self.rank)
+        self.ctx.connect(above, below, dwt2.DWT2_PEER_RANKS)
+
+    def connect_local(self, ranks: list, mode=None):
+        """Ranks of one process (this object is ranks[self.rank])."""
+        from . import dwt2
+        above, below = peer_neighbours([r.export() for r in ranks], self.rank)
+        self.ctx.connect(above, below, dwt2.DWT2_PEER_SEQUENTIAL if mode is None else mode)
+
+    def step(self, stream=None):
+        """One step of every level (concurrent ranks, one per GPU)."""
+        return self.ctx.forward(self.out, stream)
+
+    def status(self) -> int:
+        return self.ctx.status()
+
+    def close(self):
+        self.ctx.close()
+        self.plan.close()
+
+
+def sequential_step(ranks: list, stream=None):
+    """One step of emulated ranks in one stream: for each level, every rank's
+    INTERIOR part (each publishes its level-k ready flag), then every rank's
+    BOUNDARY part -- so no kernel ever waits on a later launch."""
+    from . import dwt2
+    for k in range(ranks[0].levels):
+        for r in ranks:
+            r.ctx.level(k, dwt2.DWT2_STRIP_INTERIOR, r.out, stream)
+        for r in ranks:
+            r.ctx.level(k, dwt2.DWT2_STRIP_BOUNDARY, r.out, stream)

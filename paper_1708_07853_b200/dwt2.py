@@ -15,7 +15,8 @@ import os
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libdwt2.so")      # the in-tree product library (no environment override)
 
-DWT2_OK, DWT2_EINVAL, DWT2_ENOMEM, DWT2_ECUDA, DWT2_EUNSUPPORTED = 0, -1, -2, -3, -4
+DWT2_OK, DWT2_EINVAL, DWT2_ENOMEM, DWT2_ECUDA, DWT2_EUNSUPPORTED, DWT2_ETIMEOUT = 0, -1, -2, -3, -4, -5
+DWT2_PEER_RANKS, DWT2_PEER_SEQUENTIAL = 0, 1
 DWT2_BOUNDARY_SYMMETRIC = 0
 DWT2_STRIP_ALL, DWT2_STRIP_INTERIOR, DWT2_STRIP_BOUNDARY = 0, 1, 2
 DWT2_WAVELET_CDF53, DWT2_WAVELET_CDF97, DWT2_WAVELET_CDF53_K2, DWT2_WAVELET_LIFTING = 0, 1, 2, 3
@@ -40,6 +41,23 @@ class PlanInfo(ctypes.Structure):
                 ("algorithmic_bytes", _I64), ("scratch_bytes", _I64)]
 
 
+class PeerDesc(ctypes.Structure):
+    """dwt2_peer_desc_t: what a neighbour needs to map a peer strip context."""
+    _fields_ = [("ipc_handle", ctypes.c_uint8 * 64), ("base", ctypes.c_uint64), ("pid", _I64),
+                ("device", _I32), ("width", _I32), ("global_height", _I32), ("levels", _I32),
+                ("row_begin", _I32), ("row_end", _I32), ("timeout_ms", _I32), ("reserved", _I32),
+                ("owned_off", _I64 * 32), ("pitch", _I64 * 32), ("flags_off", _I64)]
+
+    def to_bytes(self) -> bytes:
+        return bytes(self)
+
+    @classmethod
+    def from_bytes(cls, b: bytes) -> "PeerDesc":
+        if len(b) != ctypes.sizeof(cls):
+            raise ValueError(f"peer descriptor: {len(b)} bytes, expected {ctypes.sizeof(cls)}")
+        return cls.from_buffer_copy(b)
+
+
 SIGNATURES = {
     "dwt2_plan_create": (_P, [_I32, _I32, _I32, _I32]),
     "dwt2_plan_create_batched": (_P, [_I32, _I32, _I32, _I32, _I32]),
@@ -53,6 +71,14 @@ SIGNATURES = {
     "dwt2_forward_batched": (_I32, [_P, _P, _P, _I32, _I64, _I64, _P]),
     "dwt2_forward_strip": (_I32, [_P, _P, _P, _I32, _P]),
     "dwt2_forward_host": (_I32, [_P, _P, _P, _P]),
+    "dwt2_peer_strip_create": (_P, [_P, _I32]),
+    "dwt2_peer_strip_buffer": (_I32, [_P, _I32, ctypes.POINTER(_P), ctypes.POINTER(_I64)]),
+    "dwt2_peer_strip_export": (_I32, [_P, ctypes.POINTER(PeerDesc)]),
+    "dwt2_peer_strip_connect": (_I32, [_P, ctypes.POINTER(PeerDesc), ctypes.POINTER(PeerDesc), _I32]),
+    "dwt2_peer_strip_level": (_I32, [_P, _I32, _I32, _P, _P]),
+    "dwt2_peer_strip_forward": (_I32, [_P, _P, _P]),
+    "dwt2_peer_strip_status": (_I32, [_P]),
+    "dwt2_peer_strip_destroy": (None, [_P]),
     "dwt2_inverse": (_I32, [_P, _P, _P, _P]),
     "dwt2_inverse_batched": (_I32, [_P, _P, _P, _I32, _I64, _I64, _P]),
     "dwt2_scheme_steps": (_I32, [_I32]),
@@ -177,6 +203,46 @@ def dwt2_forward_strip(plan, in_ptr, out_ptr, part, stream):
 
 def dwt2_forward_host(plan, host_in_ptr, host_out_ptr, stream):
     _check(lib().dwt2_forward_host(plan, host_in_ptr, host_out_ptr, stream), "dwt2_forward_host")
+
+
+def dwt2_peer_strip_create(plan, timeout_ms=0):
+    return _plan_or_raise(lib().dwt2_peer_strip_create(plan, timeout_ms), "dwt2_peer_strip_create")
+
+
+def dwt2_peer_strip_buffer(ctx, level):
+    """(device pointer of level's first owned row, row pitch in floats)"""
+    ptr, pitch = _P(), _I64()
+    _check(lib().dwt2_peer_strip_buffer(ctx, level, ctypes.byref(ptr), ctypes.byref(pitch)),
+           "dwt2_peer_strip_buffer")
+    return ptr.value, pitch.value
+
+
+def dwt2_peer_strip_export(ctx) -> PeerDesc:
+    d = PeerDesc()
+    _check(lib().dwt2_peer_strip_export(ctx, ctypes.byref(d)), "dwt2_peer_strip_export")
+    return d
+
+
+def dwt2_peer_strip_connect(ctx, above, below, mode):
+    _check(lib().dwt2_peer_strip_connect(ctx, None if above is None else ctypes.byref(above),
+                                         None if below is None else ctypes.byref(below), mode),
+           "dwt2_peer_strip_connect")
+
+
+def dwt2_peer_strip_level(ctx, level, part, out_ptr, stream):
+    _check(lib().dwt2_peer_strip_level(ctx, level, part, out_ptr, stream), "dwt2_peer_strip_level")
+
+
+def dwt2_peer_strip_forward(ctx, out_ptr, stream):
+    _check(lib().dwt2_peer_strip_forward(ctx, out_ptr, stream), "dwt2_peer_strip_forward")
+
+
+def dwt2_peer_strip_status(ctx):
+    return lib().dwt2_peer_strip_status(ctx)
+
+
+def dwt2_peer_strip_destroy(ctx):
+    lib().dwt2_peer_strip_destroy(ctx)
 
 
 def dwt2_inverse(plan, in_ptr, out_ptr, stream):
@@ -369,6 +435,66 @@ class StripPlan:
         if getattr(self, "_p", None):
             dwt2_destroy(self._p)
             self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ of a float32 region the C library owns (torch.as_tensor wraps it)."""
+
+    def __init__(self, ptr, rows, cols, pitch):
+        self.__cuda_array_interface__ = {"shape": (rows, cols), "typestr": "<f4", "data": (ptr, False),
+                                         "strides": (pitch * 4, 4), "version": 3}
+
+
+class PeerStrip:
+    """A peer strip context (include/dwt2.h): the rank's level buffers and
+    flags in one device allocation; the halo of every level is read from the
+    neighbours' contexts by the BOUNDARY kernels (no message exchange)."""
+
+    def __init__(self, plan: StripPlan, timeout_ms: int = 0):
+        self.plan = plan                      # the C context points at the plan: keep it alive
+        self._c = dwt2_peer_strip_create(plan.handle, timeout_ms)
+
+    @property
+    def handle(self):
+        return self._c
+
+    def owned(self, level: int):
+        """torch view of level's owned rows (level 0: write the strip's pixels here)."""
+        import torch
+        info = self.plan.level_info[level]
+        ptr, pitch = dwt2_peer_strip_buffer(self._c, level)
+        arr = _DeviceArray(ptr, info.row_end - info.row_begin, info.width, pitch)
+        return torch.as_tensor(arr, device=torch.device("cuda", torch.cuda.current_device()))
+
+    def export(self) -> PeerDesc:
+        return dwt2_peer_strip_export(self._c)
+
+    def connect(self, above, below, mode=DWT2_PEER_RANKS):
+        dwt2_peer_strip_connect(self._c, above, below, mode)
+
+    def level(self, level, part, out, stream=None):
+        _check_image(out, "out")
+        dwt2_peer_strip_level(self._c, level, part, out.data_ptr(), _stream_handle(stream))
+        return out
+
+    def forward(self, out, stream=None):
+        _check_image(out, "out")
+        dwt2_peer_strip_forward(self._c, out.data_ptr(), _stream_handle(stream))
+        return out
+
+    def status(self) -> int:
+        return dwt2_peer_strip_status(self._c)
+
+    def close(self):
+        if getattr(self, "_c", None):
+            dwt2_peer_strip_destroy(self._c)
+            self._c = None
 
     def __del__(self):
         try:

@@ -1,0 +1,5 @@
+# Peer-memory halo strips: GPU tests, the emulated per-rank cost, the N=1 bench still intact
+set -x
+mkdir -p gpurun_out/peer
+timeout 900 python -m pytest tests/test_gpu_peer_strips.py -q -x 2>&1 | tail -15
+timeout 900 python scripts/r2/peer_scaling.py 2>&1 | tee gpurun_out/peer/peer_scaling.log | tail -20

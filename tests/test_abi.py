@@ -81,3 +81,25 @@ def test_oracle_not_imported_by_product():
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "dwt53_oracle" not in txt, f
+
+
+def test_peer_desc_layout_matches_header(tmp_path):
+    """dwt2_peer_desc_t crosses process boundaries as raw bytes (all_gather of
+    the descriptor): the ctypes mirror must have the C layout exactly."""
+    src = tmp_path / "desc.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "dwt2.h"\n'
+                   'int main(void) { printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(dwt2_peer_desc_t), '
+                   'offsetof(dwt2_peer_desc_t, base), offsetof(dwt2_peer_desc_t, pid), '
+                   'offsetof(dwt2_peer_desc_t, row_begin), offsetof(dwt2_peer_desc_t, owned_off), '
+                   'offsetof(dwt2_peer_desc_t, flags_off)); return 0; }\n')
+    exe = tmp_path / "desc"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    D = dwt2.PeerDesc
+    assert got == [ctypes.sizeof(D), D.base.offset, D.pid.offset, D.row_begin.offset, D.owned_off.offset,
+                   D.flags_off.offset]
+    d = D()
+    d.row_begin, d.flags_off = 128, 4096
+    assert D.from_bytes(d.to_bytes()).flags_off == 4096
+    with pytest.raises(ValueError):
+        D.from_bytes(b"\0" * 10)

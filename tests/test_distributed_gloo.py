@@ -271,3 +271,73 @@ def test_strip_pyramid_step_gloo(world, W, H, L):
         assert p.exitcode == 0
     for rank, calls in res:
         assert calls == [(k, part) for _ in range(2) for k in range(L) for part in (1, 2)]
+
+
+# ---- peer-memory halo: descriptor exchange (the GPU side is test_gpu_peer_strips.py)
+
+def _fake_desc(W, H, rank, world, L):
+    """The geometry fields dwt2_peer_strip_export fills (no GPU here)."""
+    from paper_1708_07853_b200 import dwt2
+    d = dwt2.PeerDesc()
+    d.width, d.global_height, d.levels = W, H, L
+    d.row_begin, d.row_end = D.strip_rows_levels(H, rank, world, L)
+    d.pid, d.device, d.base = os.getpid(), rank, 0x7f0000000000 + rank * (1 << 30)
+    for k, (w, h, rb, re, gt, gb) in enumerate(D.level_rows(W, H, d.row_begin, d.row_end, L)):
+        d.pitch[k] = -(-w // 4) * 4
+        d.owned_off[k] = 4096 * k + gt * 4 * d.pitch[k]
+    return d
+
+
+def _peer_worker(rank, world, port, W, H, L, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        descs = D.gather_descriptors(_fake_desc(W, H, rank, world, L).to_bytes())
+        above, below = D.peer_neighbours(descs, rank)
+        q.put((rank, None if above is None else (above.row_begin, above.row_end, above.pid, above.device),
+               None if below is None else (below.row_begin, below.row_end, below.pid, below.device), os.getpid()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,W,H,L", [(2, 64, 64, 1), (3, 100, 1030, 4), (4, 33, 97, 2)])
+def test_peer_descriptor_exchange_gloo(world, W, H, L):
+    """Every rank gets the descriptor of the rank owning the rows just above
+    (None for rank 0) and just below (None for the last rank), in the process
+    that exported it (its pid and device travel with it)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, W, H, L, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {r: (a, b, pid) for r, a, b, pid in (q.get(timeout=120) for _ in range(world))}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        a, b, _ = res[r]
+        lo, hi = D.strip_rows_levels(H, r, world, L)
+        if r == 0:
+            assert a is None
+        else:
+            assert a == (*D.strip_rows_levels(H, r - 1, world, L), res[r - 1][2], r - 1) and a[1] == lo
+        if r == world - 1:
+            assert b is None
+        else:
+            assert b == (*D.strip_rows_levels(H, r + 1, world, L), res[r + 1][2], r + 1) and b[0] == hi
+
+
+def test_peer_neighbours_rejects_mismatched_geometry():
+    descs = [_fake_desc(64, 64, r, 3, 2).to_bytes() for r in range(3)]
+    above, below = D.peer_neighbours(descs, 1)
+    assert (above.row_end, below.row_begin) == D.strip_rows_levels(64, 1, 3, 2)
+    bad = _fake_desc(64, 64, 2, 3, 2)
+    bad.row_begin += 4                      # a gap between rank 1 and rank 2
+    with pytest.raises(ValueError):
+        D.peer_neighbours([descs[0], descs[1], bad.to_bytes()], 1)
+    bad = _fake_desc(64, 64, 0, 3, 2)
+    bad.levels = 3
+    with pytest.raises(ValueError):
+        D.peer_neighbours([bad.to_bytes(), descs[1], descs[2]], 1)
