@@ -81,7 +81,8 @@ enum {
 enum {                         /* dwt2_forward_strip `part` */
     DWT2_STRIP_ALL = 0,        /* every quad row of the strip */
     DWT2_STRIP_INTERIOR = 1,   /* quad rows that read no ghost row */
-    DWT2_STRIP_BOUNDARY = 2    /* the first and the last quad row (read ghost rows) */
+    DWT2_STRIP_BOUNDARY = 2,   /* the first and the last quad row (read ghost rows) */
+    DWT2_STRIP_PUBLISH = 3     /* peer strips only: publish the level's ready flag (dwt2_peer_strip_level) */
 };
 
 /* Plan for a single W x H image, `levels` levels (1 <= levels, and every
@@ -213,22 +214,24 @@ int32_t dwt2_forward_strip(const dwt2_plan *plan, const float *in, float *out, i
  * stream-ordered sequence of 2 launches per level (CUDA-graph capturable).
  *
  * Synchronisation (flags in the context's own device memory, epochs counted
- * on the device): the INTERIOR launch of level 0 advances the rank's epoch e;
- * the INTERIOR launch of every level k publishes ready[k] = e once it runs
- * (the level-k input rows are final: they were written by level k-1, or by
- * the caller for k = 0); the BOUNDARY launch of level k waits until each
- * neighbour's ready[k] >= e, then reads its rows.  The last level's BOUNDARY
- * launch publishes done = e and, in DWT2_PEER_RANKS mode, waits until each
- * neighbour's done >= e, so when a step has completed on a rank's stream no
- * neighbour still reads that rank's buffers: the caller may then rewrite the
- * level-0 rows, and the next step may overwrite every level.  A wait that
- * exceeds the context's timeout gives up (the step's output is then invalid)
- * and latches DWT2_ETIMEOUT, reported by dwt2_peer_strip_status. */
+ * on the device): the first launch of level k publishes ready[k] = e once it
+ * runs (after griddepcontrol.wait: the rank's earlier launches are complete,
+ * so the level's input rows are final -- written by level k-1, or by the
+ * caller before the step for k = 0); the first level-0 launch of a step
+ * advances the epoch e.  A boundary quad row of level k waits until each
+ * neighbour's ready[k] >= e, then reads the neighbour's rows.  The boundary
+ * CTAs of the last level publish done = e and, in DWT2_PEER_RANKS mode, wait
+ * until each neighbour's done >= e, so when a step has completed on a rank's
+ * stream no neighbour still reads that rank's buffers: the caller may then
+ * rewrite the level-0 rows, and the next step may overwrite every level.  A
+ * wait that exceeds the context's timeout gives up (the step's output is then
+ * invalid) and latches DWT2_ETIMEOUT, reported by dwt2_peer_strip_status. */
 
 enum {
     DWT2_PEER_RANKS = 0,       /* one rank per GPU (or process), running concurrently */
-    DWT2_PEER_SEQUENTIAL = 1   /* every rank in one process and stream order: for each level, all ranks'
-                                  INTERIOR parts, then all ranks' BOUNDARY parts (1-GPU emulation);
+    DWT2_PEER_SEQUENTIAL = 1   /* every rank in one process and one stream (1-GPU emulation): per level,
+                                  every rank's PUBLISH then every rank's ALL, or every rank's INTERIOR then
+                                  every rank's BOUNDARY -- a wait is then always met by an earlier launch;
                                   no end-of-step wait; dwt2_peer_strip_forward is rejected */
 };
 
@@ -279,18 +282,25 @@ int32_t dwt2_peer_strip_export(const dwt2_peer_strip *ctx, dwt2_peer_desc_t *des
 int32_t dwt2_peer_strip_connect(dwt2_peer_strip *ctx, const dwt2_peer_desc_t *above,
                                 const dwt2_peer_desc_t *below, int32_t mode);
 
-/* One part of level k of a step: DWT2_STRIP_INTERIOR (the fused level kernel
- * on the quad rows that read no neighbour row; level 0 also advances the
- * epoch) or DWT2_STRIP_BOUNDARY (waits for the neighbours, then computes the
- * first / last quad row from the neighbours' rows in peer memory).  Parts
- * must be issued in the order INTERIOR(0), BOUNDARY(0), INTERIOR(1), ... on
- * one stream of each rank.  out: the strip-local Mallat pyramid (W x (row_end
- * - row_begin), pitch W, device), as dwt2_forward_strip_level writes it. */
+/* Level k of a step, on `stream`, after level k-1:
+ *   DWT2_STRIP_ALL       ONE launch: the fused level kernel on the interior
+ *                        quad rows plus boundary-role CTAs that wait for the
+ *                        neighbours and compute the first / last quad row from
+ *                        their rows in peer memory (the step's form);
+ *   DWT2_STRIP_INTERIOR  the level kernel on the interior quad rows only, then
+ *   DWT2_STRIP_BOUNDARY  the boundary quad rows in a launch of their own.
+ *   DWT2_STRIP_PUBLISH   only publishes ready[k] (a 1-thread launch): the
+ *                        sequential emulation issues it for every rank before
+ *                        the ranks' ALL launches of the level.
+ * For one level use ALL, or INTERIOR then BOUNDARY.  out: the strip-local
+ * Mallat pyramid (W x (row_end - row_begin), pitch W, device), as
+ * dwt2_forward_strip_level writes it.  A rank without neighbours runs every
+ * quad row in one level launch (BOUNDARY is then a no-op). */
 int32_t dwt2_peer_strip_level(dwt2_peer_strip *ctx, int32_t level, int32_t part, float *out,
                               dwt2_stream_t stream);
 
-/* A whole step (every level, both parts; 2 launches per level, no host
- * synchronisation).  DWT2_PEER_RANKS mode only. */
+/* A whole step: one DWT2_STRIP_ALL launch per level (no host
+ * synchronisation; capturable in a CUDA graph).  DWT2_PEER_RANKS mode only. */
 int32_t dwt2_peer_strip_forward(dwt2_peer_strip *ctx, float *out, dwt2_stream_t stream);
 
 /* DWT2_OK, or DWT2_ETIMEOUT once any flag wait of this context has timed out

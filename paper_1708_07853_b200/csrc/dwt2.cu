@@ -102,6 +102,9 @@ namespace {
 #ifndef DWT2_NO_GRP                        // probes only: no row-grouped TMA (bulk-copy loader instead)
 #define DWT2_NO_GRP 0
 #endif
+#ifndef DWT2_PROBE_NOWAIT                  // probes only (WRONG results): levels >= 2 skip griddepcontrol.wait at entry
+#define DWT2_PROBE_NOWAIT 0                 // (they wait at exit), to bound what overlapping a level's drain with
+#endif                                      // the next level's start could save
 #ifndef DWT2_FORCE_SCALAR                   // probes only: scalar subband stores everywhere
 #define DWT2_FORCE_SCALAR 0
 #endif
@@ -191,8 +194,10 @@ struct alignas(64) LevelArgs {
     long long flat_rows;              // GRP: count * in_rows
     int rev;                          // 1: images and quad rows in reverse order (tile t -> mirrored rows)
     int rsum;                         // rev: qa0 + the end of the level's quad rows (mirror q -> rsum - q)
-    unsigned int *peer_flags;         // peer strip context (peer.cu): publish ready[peer_level] at entry, else null
-    int peer_level;
+    int nowait;                       // DWT2_PROBE_NOWAIT builds only
+    int peer;                         // peer strip launch (peer.cu): publish pb.level's ready flag at entry
+    int pb_ctas;                      // the last pb_ctas CTAs of the grid take the boundary role
+    PeerBoundaryArgs pb;
 };
 
 // Row-grouped TMA (GRP) for row pitches that are not a multiple of 16 bytes:
@@ -771,10 +776,19 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
     const unsigned long long t_entry = gtimer();
 #endif
     pdl_launch_dependents();
-    pdl_wait();
-    // peer strip step (peer.cu): every earlier level of this rank is complete
-    // here, so this level's input rows are final -- tell the neighbours
-    if (a.peer_flags != nullptr && blockIdx.x == 0 && threadIdx.x == 0) peer_publish_ready(a.peer_flags, a.peer_level);
+    if (!DWT2_PROBE_NOWAIT || !a.nowait) pdl_wait();
+    // peer strip launch (peer.cu): every earlier launch of this rank's step is
+    // complete, so this level's input rows are final -- tell the neighbours;
+    // in a fused launch the CTAs past the level's own grid compute the strip's
+    // boundary quad rows from the neighbours' memory
+    if (a.peer && blockIdx.x == 0 && threadIdx.x == 0) peer_publish(a.pb.flags, a.pb.level);
+    if (a.pb_ctas > 0 && int(blockIdx.x) >= int(gridDim.x) - a.pb_ctas) {
+        const int c = int(blockIdx.x) - (int(gridDim.x) - a.pb_ctas);
+        peer_boundary_role(a.pb, c % a.pb.nbx, c / a.pb.nbx, reinterpret_cast<float *>(smem_raw));
+        __syncthreads();
+        if (threadIdx.x == 0) peer_exit(a.pb);
+        return;
+    }
 #ifdef DWT2_PROF
     if (threadIdx.x == 0 && blockIdx.x < 4096) {
         unsigned smid;
@@ -1071,6 +1085,7 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
             issue_next();
         }
     }
+    if (DWT2_PROBE_NOWAIT && a.nowait) pdl_wait();
 #ifdef DWT2_PROF
     if (lane == 0) {
         atomicAdd(&g_prof[0], (unsigned long long)t_wait);
@@ -1140,8 +1155,8 @@ struct LaunchIO {
     long long out_pitch, out_img_stride;
     int out_q0, hq_local;     // strip-local quad row 0, LL rows present in out (LH offset)
     int count;
-    unsigned int *peer_flags; // peer strip INTERIOR launches: the rank's flag block (else null)
-    int peer_level;
+    const PeerBoundaryArgs *peer;   // fused peer strip launch (else null) and its boundary-role CTAs
+    int peer_ctas;
 };
 
 // Tile-size policy of the work queue (measured on B200).
@@ -1201,11 +1216,15 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     a.nslabs = (W + SLAB - 1) / SLAB;
     a.count = io.count;
     a.qa0 = qa0; a.qa1 = qa1; a.qb0 = qb0; a.qb1 = qb1;
-    a.peer_flags = io.peer_flags;
-    a.peer_level = io.peer_level;
+    a.nowait = (DWT2_PROBE_NOWAIT && level >= 1 && queue == 0) ? 1 : 0;
+    if (io.peer) {
+        a.peer = 1;
+        a.pb = *io.peer;
+        a.pb_ctas = io.peer_ctas;
+    }
     const int lenA = qa1 - qa0, lenB = qb1 - qb0;
     const long long slab_rows = (long long)io.count * a.nslabs * (lenA + lenB);
-    if (slab_rows == 0) return io.peer_flags ? launch_peer_publish(io.peer_flags, io.peer_level, stream) : DWT2_OK;
+    if (slab_rows == 0) return io.peer ? fail(DWT2_EINVAL) : DWT2_OK;      // peer.cu launches no empty level
 
     const bool tma = !DWT2_FORCE_GENERIC && aligned(io.in, 16) && (io.in_pitch * 4) % 16 == 0 &&
                      (io.count == 1 || (io.in_img_stride * 4) % 16 == 0);
@@ -1353,7 +1372,7 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     }
 
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = dim3(grid + a.pb_ctas);
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = grp ? RingG<true, 2>::SMEM : s3 ? Ring<true, S_LARGE>::SMEM : tma ? Ring<true>::SMEM : Ring<false>::SMEM;
     cfg.stream = stream;
@@ -1819,7 +1838,8 @@ int32_t dwt2_strip_level_info(const dwt2_plan *p, int32_t level, dwt2_strip_leve
 namespace dwt2_detail {
 
 int32_t strip_level_launch(const dwt2_plan *p, int level, const float *in, long long in_pitch, float *ll_out,
-                           long long ll_pitch, float *out, int part, cudaStream_t stream, unsigned int *peer_flags)
+                           long long ll_pitch, float *out, int part, cudaStream_t stream,
+                           const PeerBoundaryArgs *peer, int peer_ctas)
 {
     dwt2_strip_level_t L;
     if (!p || !in || !out || !p->strip || part < 0 || part > 2 || !aligned(in, 4) || !aligned(out, 4) ||
@@ -1863,8 +1883,8 @@ int32_t strip_level_launch(const dwt2_plan *p, int level, const float *in, long 
         io.ll_pitch = ll_pitch;
     }
     io.ll_img_stride = io.ll_pitch * (qe - qs);
-    io.peer_flags = peer_flags;
-    io.peer_level = level;
+    io.peer = peer;
+    io.peer_ctas = peer_ctas;
     const int ia = qs + (L.ghost_top ? 1 : 0), ib = qe - (L.ghost_bot ? 1 : 0);
     int a0, a1, b0 = 0, b1 = 0;
     if (part == DWT2_STRIP_ALL) {
@@ -1886,6 +1906,11 @@ int32_t strip_level_launch(const dwt2_plan *p, int level, const float *in, long 
     return DWT2_OK;
 }
 
+int level_kernel_threads() { return THREADS; }
+
+// a boundary-role CTA of a fused peer launch stages 5 rows of 2 THREADS + 4 floats in the ring's smem
+static_assert(5 * (2 * THREADS + 4) * sizeof(float) <= Ring<false>::SMEM, "boundary role tile exceeds the ring");
+
 }  // namespace dwt2_detail
 
 extern "C" {
@@ -1894,7 +1919,7 @@ int32_t dwt2_forward_strip_level(const dwt2_plan *p, int32_t level, const float 
                                  float *ll_out, int64_t ll_pitch, float *out, int32_t part, dwt2_stream_t stream)
 {
     return strip_level_launch(p, level, in, in_pitch, ll_out, ll_pitch, out, part,
-                              reinterpret_cast<cudaStream_t>(stream), nullptr);
+                              reinterpret_cast<cudaStream_t>(stream));
 }
 
 int32_t dwt2_forward_strip(const dwt2_plan *p, const float *in, float *out, int32_t part, dwt2_stream_t stream)

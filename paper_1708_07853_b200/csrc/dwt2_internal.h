@@ -130,35 +130,200 @@ struct dwt2_plan {
 namespace dwt2_detail {
 
 // ---- peer strip contexts (peer.cu): flag block layout (uint32 words)
-constexpr int PEER_EPOCH = 0;        // the rank's step epoch (advanced by the level-0 INTERIOR launch)
-constexpr int PEER_DONE = 1;         // epoch whose last-level BOUNDARY launch has finished reading the neighbours
+constexpr int PEER_EPOCH = 0;        // the rank's step epoch (advanced by the first launch of level 0)
+constexpr int PEER_DONE = 1;         // epoch whose last level has finished reading the neighbours
 constexpr int PEER_ERR = 2;          // nonzero: a flag wait timed out
-constexpr int PEER_CTR = 3;          // BOUNDARY CTAs finished (last level; self-resetting)
+constexpr int PEER_CTR = 3;          // boundary-role CTAs of the current launch that finished (self-resetting)
 constexpr int PEER_READY = 8;        // + k: epoch whose level-k input rows are final
 constexpr int PEER_FLAG_WORDS = PEER_READY + MAX_LEVELS;
 
+// The boundary quad rows of one level of a peer strip (the first and / or the
+// last quad row of the strip, whose 5 x 5 windows reach into the neighbours'
+// rows), computed by boundary-role CTAs: the CTAs past the level kernel's own
+// grid in a fused launch, or the whole grid of peer.cu's boundary kernel.
+struct PeerBoundaryArgs {
+    const float *own;                 // global row rb of this rank (level k)
+    const float *up;                  // global row rb - 2 in the rank above (null: none)
+    const float *dn;                  // global row re in the rank below (null: none)
+    long long own_pitch, up_pitch, dn_pitch;
+    const unsigned int *up_flags, *dn_flags;
+    unsigned int *flags;              // this rank's flag block
+    float *ll;                        // LL row of quad row qs
+    float *hl, *lh, *hh;              // subband rows of quad row qs (strip-local output)
+    long long ll_pitch, out_pitch;
+    long long timeout_ns;
+    int W, H, rb, re, qs;
+    int n0, n1;                       // the boundary quad rows (global)
+    int nbx;                          // boundary-role CTAs per boundary quad row
+    int nroles;                       // boundary-role CTAs of the launch
+    int level, last;                  // last: the strip's last level (publishes done)
+    int quiesce;                      // last level: wait until the neighbours are done reading this rank
+};
+
 #ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long peer_gtime()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ unsigned peer_ld_acquire_sys(const unsigned int *p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void peer_st_release_sys(unsigned int *p, unsigned v)
+{
+#ifdef DWT2_PEER_FENCE_GPU      // probe builds only: device-scope release (ranks on one GPU)
+    asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#else
+    asm volatile("fence.acq_rel.sys;\n\tst.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#endif
+}
+
 // Publish "level `level` input rows of this rank are final for the current
-// epoch" (one thread, after griddepcontrol.wait: every earlier launch of the
-// rank's step has completed and its writes are visible).  Level 0 advances
-// the epoch.  The system-scope fence makes those writes visible to a peer GPU
-// that acquires the flag over NVLink before it reads the rows.
-__device__ __forceinline__ void peer_publish_ready(unsigned int *f, int level)
+// epoch": one thread of the first launch of the level, after
+// griddepcontrol.wait (every earlier launch of the rank's step has completed
+// and its writes are visible; the system-scope release carries them to a peer
+// GPU that acquires the flag over NVLink).  The first publish of level 0 in a
+// step (epoch == done) advances the epoch; publishing again is a no-op.
+static __device__ __noinline__ void peer_publish(unsigned int *f, int level)
 {
     volatile unsigned int *vf = f;
     unsigned e = vf[PEER_EPOCH];
-    if (level == 0) vf[PEER_EPOCH] = ++e;
-    __threadfence_system();
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f + PEER_READY + level), "r"(e) : "memory");
+    if (level == 0 && e == vf[PEER_DONE]) vf[PEER_EPOCH] = ++e;
+    peer_st_release_sys(f + PEER_READY + level, e);
+}
+
+// spin until *f >= e (epochs compared modulo 2^32); latches PEER_ERR and gives
+// up after timeout_ns (no hang if a neighbour never arrives)
+static __device__ __noinline__ void peer_wait_epoch(const unsigned int *f, unsigned e, const PeerBoundaryArgs &a)
+{
+    const unsigned long long t0 = peer_gtime();
+    while (int(peer_ld_acquire_sys(f) - e) < 0) {
+        if ((long long)(peer_gtime() - t0) > a.timeout_ns) {
+            atomicExch(a.flags + PEER_ERR, 1u);
+            return;
+        }
+        __nanosleep(100);
+    }
+}
+
+// this step's epoch: once the level-0 publish of the step has run, epoch =
+// done + 1 (a boundary-role CTA of level 0 may start before the CTA that
+// publishes; it waits for it)
+static __device__ __noinline__ unsigned peer_epoch(const PeerBoundaryArgs &a)
+{
+    volatile const unsigned int *vf = a.flags;
+    const unsigned long long t0 = peer_gtime();
+    unsigned e;
+    while ((e = vf[PEER_EPOCH]) != vf[PEER_DONE] + 1u) {
+        if ((long long)(peer_gtime() - t0) > a.timeout_ns) {
+            atomicExch(a.flags + PEER_ERR, 1u);
+            break;
+        }
+        __nanosleep(100);
+    }
+    return e;
+}
+
+// whole-sample symmetric reflection for k in [-2, n + 1], n >= 2
+__device__ __forceinline__ int peer_wss2(int k, int n)
+{
+    k = k < 0 ? -k : k;
+    return k >= n ? 2 * (n - 1) - k : k;
+}
+
+// One boundary-role CTA: blockDim.x quads of boundary quad row (by ? n1 : n0)
+// from quad bx * blockDim.x.  tile: 5 x (2 blockDim.x + 4) floats of smem.
+// Waits (thread 0) for the neighbours' level-k ready flags, stages the 5 input
+// rows -- the neighbours' from their memory -- and evaluates the 2-D analysis
+// filters pointwise: h = (-1/8, 1/4, 3/4, 1/4, -1/8) at even, g = (-1/2, 1, -1/2)
+// at odd positions, row pass then column pass in fp64 (Eq. (4), PAPER.md
+// L160-171, which the lifting steps of Eq. (5) reach exactly: every product and
+// sum here is exact for fp32 data, so the stored fp32 is the level kernel's).
+static __device__ __noinline__ void peer_boundary_role(const PeerBoundaryArgs &a, int bx, int by, float *tile)
+{
+    const int nt = blockDim.x, cols = 2 * nt + 4;
+    if (threadIdx.x == 0) {
+        const unsigned e = peer_epoch(a);
+        if (a.up_flags) peer_wait_epoch(a.up_flags + PEER_READY + a.level, e, a);
+        if (a.dn_flags) peer_wait_epoch(a.dn_flags + PEER_READY + a.level, e, a);
+    }
+    __syncthreads();
+    const int n = by == 0 ? a.n0 : a.n1;
+    const int W = a.W, H = a.H;
+    const int Wq = (W + 1) >> 1, Wh = W >> 1, Hh = H >> 1;
+    const int m0 = bx * nt;
+    const int c0 = 2 * m0 - 2;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const int y = peer_wss2(2 * n - 2 + j, H);
+        const float *row = y < a.rb ? a.up + (long long)(y - (a.rb - 2)) * a.up_pitch
+                         : y >= a.re ? a.dn + (long long)(y - a.re) * a.dn_pitch
+                                     : a.own + (long long)(y - a.rb) * a.own_pitch;
+        for (int i = threadIdx.x; i < cols; i += nt) {
+            const int x = c0 + i;
+            if (x <= W + 1) tile[j * cols + i] = __ldcg(row + peer_wss2(x, W));
+        }
+    }
+    __syncthreads();
+    const int m = m0 + threadIdx.x;
+    if (m < Wq) {
+        double lo[5], hi[5];              // row passes: h at column 2m, g at column 2m + 1
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            const float *v = tile + j * cols + 2 * threadIdx.x;
+            const double v0 = v[0], v1 = v[1], v2 = v[2], v3 = v[3], v4 = v[4];
+            lo[j] = fma(0.75, v2, fma(0.25, v1 + v3, -0.125 * (v0 + v4)));
+            hi[j] = fma(-0.5, v2 + v4, v3);
+        }
+        const double ll = fma(0.75, lo[2], fma(0.25, lo[1] + lo[3], -0.125 * (lo[0] + lo[4])));
+        const double lh = fma(-0.5, lo[2] + lo[4], lo[3]);
+        const double hl = fma(0.75, hi[2], fma(0.25, hi[1] + hi[3], -0.125 * (hi[0] + hi[4])));
+        const double hh = fma(-0.5, hi[2] + hi[4], hi[3]);
+        const long long r = n - a.qs;
+        a.ll[r * a.ll_pitch + m] = (float)ll;
+        if (m < Wh) a.hl[r * a.out_pitch + m] = (float)hl;
+        if (n < Hh) {
+            a.lh[r * a.out_pitch + m] = (float)lh;
+            if (m < Wh) a.hh[r * a.out_pitch + m] = (float)hh;
+        }
+    }
+}
+
+// A boundary-role CTA has finished (all its stores and neighbour reads, after
+// a __syncthreads; one thread).  On the strip's last level the last role CTA
+// of the launch publishes done = epoch and, for concurrent ranks, waits until
+// both neighbours are done reading this rank's buffers.
+static __device__ __noinline__ void peer_exit(const PeerBoundaryArgs &a)
+{
+    if (!a.last) return;
+    __threadfence();
+    if (atomicAdd(a.flags + PEER_CTR, 1u) + 1u != unsigned(a.nroles)) return;
+    atomicExch(a.flags + PEER_CTR, 0u);
+    __threadfence();
+    const unsigned e = *reinterpret_cast<volatile unsigned int *>(a.flags + PEER_EPOCH);
+    peer_st_release_sys(a.flags + PEER_DONE, e);
+    if (a.quiesce) {
+        if (a.up_flags) peer_wait_epoch(a.up_flags + PEER_DONE, e, a);
+        if (a.dn_flags) peer_wait_epoch(a.dn_flags + PEER_DONE, e, a);
+    }
 }
 #endif
 
-// a one-thread launch of peer_publish_ready (strips whose INTERIOR part is empty)
-int32_t launch_peer_publish(unsigned int *flags, int level, cudaStream_t stream);
+// threads per CTA of the level kernel (quads of a boundary-role CTA in a fused launch)
+int level_kernel_threads();
 
-// dwt2_forward_strip_level with an optional peer flag block (peer.cu INTERIOR parts)
+// dwt2_forward_strip_level; with `peer` (peer.cu) the level kernel publishes
+// the level's ready flag at entry and its grid gets peer_ctas more CTAs in the
+// boundary role
 int32_t strip_level_launch(const dwt2_plan *p, int level, const float *in, long long in_pitch, float *ll_out,
-                           long long ll_pitch, float *out, int part, cudaStream_t stream, unsigned int *peer_flags);
+                           long long ll_pitch, float *out, int part, cudaStream_t stream,
+                           const PeerBoundaryArgs *peer = nullptr, int peer_ctas = 0);
 
 // ---- tail kernel (tail.cu): the small last levels of a forward in one launch
 constexpr int MAX_TAIL = 16;

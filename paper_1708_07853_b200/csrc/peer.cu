@@ -1,29 +1,27 @@
-// peer.cu -- row strips with the halo exchange fused into the boundary kernel
+// peer.cu -- row strips with the halo exchange fused into the level launch
 // (include/dwt2.h "peer strip context").
 //
 // The paper's multi-core mapping synchronises cores at the exchange of the
 // samples a step needs from a neighbouring band (section 3).
 // On an NVSwitch node the neighbour's rows are one NVLink load away, so the
-// exchange is not a message: the BOUNDARY kernel of level k acquires the
-// neighbour's level-k ready flag and reads the 2 rows above / 1 row below
-// straight from the neighbour's buffer (CUDA IPC mapping; ranks emulated in
-// one process share the device).  The INTERIOR launch of the level (the fused
-// TMA level kernel of dwt2.cu, unchanged apart from publishing the flag at
-// entry) needs no neighbour row and never waits.
+// exchange is not a message: boundary-role CTAs acquire the neighbour's
+// level-k ready flag and read the 2 rows above / 1 row below straight from the
+// neighbour's buffer (CUDA IPC mapping; ranks emulated in one process share the
+// device).  In a whole step (DWT2_STRIP_ALL) those CTAs ride in the level
+// kernel's own launch (dwt2.cu: the CTAs past its grid take the boundary role),
+// so a level is ONE launch and the exchange overlaps the interior tiles; the
+// first launch of a level publishes its ready flag at entry (dwt2_internal.h
+// peer_publish).
 //
-// The boundary quad rows are computed pointwise with the 2-D analysis
-// filters that the lifting steps of Eq. (5) reach exactly (PAPER.md
-// L160-171, Eq. (4)): h = (-1/8, 1/4, 3/4, 1/4, -1/8) on even positions,
-// g = (-1/2, 1, -1/2) on odd ones, a row pass and a column pass in fp64
-// (every product and partial sum of these dyadic taps with fp32 data is
-// exact, so the stored fp32 equals the level kernel's; tail.cu uses the same
-// evaluation).  A CTA stages the 5 input rows of 256 quads in shared memory
-// (coalesced loads: peer memory is read once per element).
+// The boundary quad rows are computed pointwise with the 2-D analysis filters
+// that the lifting steps of Eq. (5) reach exactly (Eq. (4);
+// dwt2_internal.h peer_boundary_role), bit for bit the level kernel's values.
 #include <cuda_runtime.h>
 #include <unistd.h>
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 
 #include "dwt2_internal.h"
 
@@ -49,142 +47,24 @@ struct dwt2_peer_strip {
 
 namespace {
 
-constexpr int PB_THREADS = 256;                   // quads per CTA
-constexpr int PB_COLS = 2 * PB_THREADS + 4;       // staged columns 2 m0 - 2 .. 2 m0 + 2 PB_THREADS + 1
-
-struct PeerBoundaryArgs {
-    const float *own;                 // global row rb of this rank (level k)
-    const float *up;                  // global row rb - 2 in the rank above (null: none)
-    const float *dn;                  // global row re in the rank below (null: none)
-    long long own_pitch, up_pitch, dn_pitch;
-    const unsigned int *up_flags, *dn_flags;
-    unsigned int *flags;
-    float *ll;                        // LL row of quad row qs
-    float *hl, *lh, *hh;              // subband rows of quad row qs (strip-local output)
-    long long ll_pitch, out_pitch;
-    long long timeout_ns;
-    int W, H, rb, re, qs;
-    int n0, n1;                       // the boundary quad rows (global); blockIdx.y selects
-    int level, last, quiesce;
-};
-
-__device__ __forceinline__ unsigned long long gtime()
-{
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned int *p)
-{
-    unsigned v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// spin until *f >= e (epochs compared modulo 2^32); false after timeout_ns
-__device__ bool wait_epoch(const unsigned int *f, unsigned e, long long timeout_ns)
-{
-    const unsigned long long t0 = gtime();
-    while (int(ld_acquire_sys(f) - e) < 0) {
-        if ((long long)(gtime() - t0) > timeout_ns) return false;
-        __nanosleep(100);
-    }
-    return true;
-}
-
-// whole-sample symmetric reflection for k in [-2, n + 1], n >= 2
-__device__ __forceinline__ int wss2(int k, int n)
-{
-    k = k < 0 ? -k : k;
-    return k >= n ? 2 * (n - 1) - k : k;
-}
+constexpr int PB_THREADS = 256;                   // quads per CTA of the standalone boundary kernel
 
 __global__ void __launch_bounds__(1) peer_publish_kernel(unsigned int *flags, int level)
 {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    peer_publish_ready(flags, level);
+    peer_publish(flags, level);
 }
 
 __global__ void __launch_bounds__(PB_THREADS) peer_boundary_kernel(const __grid_constant__ PeerBoundaryArgs a)
 {
-    __shared__ float tile[5][PB_COLS];
+    __shared__ float tile[5 * (2 * PB_THREADS + 4)];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const unsigned e = *reinterpret_cast<volatile unsigned int *>(a.flags + PEER_EPOCH);
-    if (threadIdx.x == 0) {
-        bool ok = true;
-        if (a.up_flags) ok = wait_epoch(a.up_flags + PEER_READY + a.level, e, a.timeout_ns) && ok;
-        if (a.dn_flags) ok = wait_epoch(a.dn_flags + PEER_READY + a.level, e, a.timeout_ns) && ok;
-        if (!ok) atomicExch(a.flags + PEER_ERR, 1u);
-    }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) peer_publish(a.flags, a.level);
+    peer_boundary_role(a, blockIdx.x, blockIdx.y, tile);
     __syncthreads();
-
-    const int n = blockIdx.y == 0 ? a.n0 : a.n1;
-    const int W = a.W, H = a.H;
-    const int Wq = (W + 1) >> 1, Wh = W >> 1, Hh = H >> 1;
-    const int m0 = blockIdx.x * PB_THREADS;
-    const int c0 = 2 * m0 - 2;
-    // stage input rows 2n-2 .. 2n+2 (mirrored at the image edges; rows outside
-    // [rb, re) come from the neighbours' memory), columns c0 .. c0 + PB_COLS - 1
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-        const int y = wss2(2 * n - 2 + j, H);
-        const float *row = y < a.rb ? a.up + (long long)(y - (a.rb - 2)) * a.up_pitch
-                         : y >= a.re ? a.dn + (long long)(y - a.re) * a.dn_pitch
-                                     : a.own + (long long)(y - a.rb) * a.own_pitch;
-        for (int i = threadIdx.x; i < PB_COLS; i += PB_THREADS) {
-            const int x = c0 + i;
-            if (x <= W + 1) tile[j][i] = __ldcg(row + wss2(x, W));
-        }
-    }
-    __syncthreads();
-
-    const int m = m0 + threadIdx.x;
-    if (m < Wq) {
-        double lo[5], hi[5];              // row passes: h at column 2m, g at column 2m + 1
-#pragma unroll
-        for (int j = 0; j < 5; ++j) {
-            const float *v = &tile[j][2 * threadIdx.x];
-            const double v0 = v[0], v1 = v[1], v2 = v[2], v3 = v[3], v4 = v[4];
-            lo[j] = fma(0.75, v2, fma(0.25, v1 + v3, -0.125 * (v0 + v4)));
-            hi[j] = fma(-0.5, v2 + v4, v3);
-        }
-        const double ll = fma(0.75, lo[2], fma(0.25, lo[1] + lo[3], -0.125 * (lo[0] + lo[4])));
-        const double lh = fma(-0.5, lo[2] + lo[4], lo[3]);
-        const double hl = fma(0.75, hi[2], fma(0.25, hi[1] + hi[3], -0.125 * (hi[0] + hi[4])));
-        const double hh = fma(-0.5, hi[2] + hi[4], hi[3]);
-        const long long r = n - a.qs;
-        a.ll[r * a.ll_pitch + m] = (float)ll;
-        if (m < Wh) a.hl[r * a.out_pitch + m] = (float)hl;
-        if (n < Hh) {
-            a.lh[r * a.out_pitch + m] = (float)lh;
-            if (m < Wh) a.hh[r * a.out_pitch + m] = (float)hh;
-        }
-    }
-
-    if (a.last) {
-        // the last CTA to finish publishes done = e (no CTA of this rank reads a
-        // neighbour any more this step) and, for concurrent ranks, waits until
-        // the neighbours are done reading this rank's buffers
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            const unsigned total = gridDim.x * gridDim.y;
-            if (atomicAdd(a.flags + PEER_CTR, 1u) == total - 1) {
-                atomicExch(a.flags + PEER_CTR, 0u);
-                __threadfence_system();
-                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.flags + PEER_DONE), "r"(e) : "memory");
-                if (a.quiesce) {
-                    bool ok = true;
-                    if (a.up_flags) ok = wait_epoch(a.up_flags + PEER_DONE, e, a.timeout_ns) && ok;
-                    if (a.dn_flags) ok = wait_epoch(a.dn_flags + PEER_DONE, e, a.timeout_ns) && ok;
-                    if (!ok) atomicExch(a.flags + PEER_ERR, 1u);
-                }
-            }
-        }
-    }
+    if (threadIdx.x == 0) peer_exit(a);
 }
 
 cudaLaunchAttribute pdl_attr()
@@ -212,27 +92,77 @@ bool same_geometry(const dwt2_peer_strip *c, const dwt2_peer_desc_t *d)
     return d->width == p->W && d->global_height == p->Hg && d->levels == p->levels && d->device >= 0;
 }
 
-}  // namespace
+// the boundary quad rows of level k and their arguments (returns their count, 0: none)
+int boundary_args(const dwt2_peer_strip *c, int level, float *out, PeerBoundaryArgs *a)
+{
+    const dwt2_plan *p = c->plan;
+    const dwt2_strip_level_t &L = c->info[level];
+    const bool last = level == c->levels - 1;
+    // [qs, ia) and [max(ib, ia), qe), as dwt2_forward_strip_level splits a level
+    const int qs = L.row_begin / 2, qe = (L.row_end + 1) / 2;
+    const int ia = qs + (L.ghost_top ? 1 : 0), ib = qe - (L.ghost_bot ? 1 : 0);
+    int rows[2], nr = 0;
+    if (ia > qs) rows[nr++] = qs;
+    if (std::max(ib, ia) < qe) rows[nr++] = qe - 1;
+    memset(a, 0, sizeof(*a));
+    if (nr == 0) return 0;
+    a->own = reinterpret_cast<const float *>(c->base + c->own_off[level]);
+    a->own_pitch = c->pitch[level];
+    if (L.ghost_top) {
+        const dwt2_peer_desc_t &d = c->nb[0];
+        int rb, re;
+        level_rows(d.row_begin, d.row_end, level, &rb, &re);
+        a->up = reinterpret_cast<const float *>(c->nb_base[0] + d.owned_off[level]) + (long long)(re - rb - 2) * d.pitch[level];
+        a->up_pitch = d.pitch[level];
+        a->up_flags = reinterpret_cast<const unsigned int *>(c->nb_base[0] + d.flags_off);
+    }
+    if (L.ghost_bot) {
+        const dwt2_peer_desc_t &d = c->nb[1];
+        a->dn = reinterpret_cast<const float *>(c->nb_base[1] + d.owned_off[level]);
+        a->dn_pitch = d.pitch[level];
+        a->dn_flags = reinterpret_cast<const unsigned int *>(c->nb_base[1] + d.flags_off);
+    }
+    a->flags = c->flags();
+    // output bases as the level kernel's (dwt2.cu launch_level): level k's
+    // subbands start at row 0 of the strip-local pyramid (pitch W)
+    const int Wq = (L.width + 1) / 2;
+    a->ll = last ? out : reinterpret_cast<float *>(c->base + c->own_off[level + 1]);
+    a->ll_pitch = last ? p->W : c->pitch[level + 1];
+    a->hl = out + Wq;
+    a->lh = out + (long long)(qe - qs) * p->W;
+    a->hh = a->lh + Wq;
+    a->out_pitch = p->W;
+    a->timeout_ns = (long long)c->timeout_ms * 1000000LL;
+    a->W = L.width;
+    a->H = L.global_height;
+    a->rb = L.row_begin;
+    a->re = L.row_end;
+    a->qs = qs;
+    a->n0 = rows[0];
+    a->n1 = rows[nr - 1];
+    a->level = level;
+    a->last = last ? 1 : 0;
+    a->quiesce = c->mode == DWT2_PEER_RANKS ? 1 : 0;
+    return nr;
+}
 
-namespace dwt2_detail {
-
-int32_t launch_peer_publish(unsigned int *flags, int level, cudaStream_t stream)
+int32_t launch_boundary(const PeerBoundaryArgs &a, int nr, cudaStream_t s)
 {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(1);
-    cfg.blockDim = dim3(1);
-    cfg.stream = stream;
+    cfg.gridDim = dim3(a.nbx, nr);
+    cfg.blockDim = dim3(PB_THREADS);
+    cfg.stream = s;
     cudaLaunchAttribute at = pdl_attr();
     cfg.attrs = &at;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, peer_publish_kernel, flags, level) != cudaSuccess) {
+    if (cudaLaunchKernelEx(&cfg, peer_boundary_kernel, a) != cudaSuccess) {
         cudaGetLastError();
         return fail(DWT2_ECUDA);
     }
     return DWT2_OK;
 }
 
-}  // namespace dwt2_detail
+}  // namespace
 
 extern "C" {
 
@@ -363,7 +293,7 @@ int32_t dwt2_peer_strip_connect(dwt2_peer_strip *c, const dwt2_peer_desc_t *abov
 int32_t dwt2_peer_strip_level(dwt2_peer_strip *c, int32_t level, int32_t part, float *out, dwt2_stream_t stream)
 {
     if (!c || !c->connected || level < 0 || level >= c->levels || !out || !aligned(out, 4) ||
-        (part != DWT2_STRIP_INTERIOR && part != DWT2_STRIP_BOUNDARY))
+        part < DWT2_STRIP_ALL || part > DWT2_STRIP_PUBLISH)
         return fail(DWT2_EINVAL);
     const dwt2_plan *p = c->plan;
     const size_t out_bytes = size_t(p->W) * (p->row_end - p->row_begin) * sizeof(float);
@@ -371,87 +301,55 @@ int32_t dwt2_peer_strip_level(dwt2_peer_strip *c, int32_t level, int32_t part, f
     const cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const dwt2_strip_level_t &L = c->info[level];
     const bool last = level == c->levels - 1;
+    const float *in = reinterpret_cast<const float *>(c->base + c->buf_off[level]);
     float *ll_out = last ? nullptr : reinterpret_cast<float *>(c->base + c->own_off[level + 1]);
     const long long ll_pitch = last ? 0 : c->pitch[level + 1];
-    if (part == DWT2_STRIP_INTERIOR) {
-        const float *in = reinterpret_cast<const float *>(c->base + c->buf_off[level]);
-        const bool alone = L.ghost_top == 0 && L.ghost_bot == 0;      // no neighbour: nothing to publish
-        return strip_level_launch(p, level, in, c->pitch[level], ll_out, ll_pitch, out, DWT2_STRIP_INTERIOR, s,
-                                  alone ? nullptr : c->flags());
-    }
-    if (L.ghost_top == 0 && L.ghost_bot == 0) return DWT2_OK;
-    // the boundary quad rows: [qs, ia) and [max(ib, ia), qe) (dwt2_forward_strip_level)
-    const int qs = L.row_begin / 2, qe = (L.row_end + 1) / 2;
-    const int ia = qs + (L.ghost_top ? 1 : 0), ib = qe - (L.ghost_bot ? 1 : 0);
-    int rows[2], nr = 0;
-    if (ia > qs) rows[nr++] = qs;
-    if (L.ghost_bot && std::max(ib, ia) < qe && !(nr == 1 && rows[0] == qe - 1)) rows[nr++] = qe - 1;
     PeerBoundaryArgs a;
-    memset(&a, 0, sizeof(a));
-    a.own = reinterpret_cast<const float *>(c->base + c->own_off[level]);
-    a.own_pitch = c->pitch[level];
-    if (L.ghost_top) {
-        const dwt2_peer_desc_t &d = c->nb[0];
-        int rb, re;
-        level_rows(d.row_begin, d.row_end, level, &rb, &re);
-        a.up = reinterpret_cast<const float *>(c->nb_base[0] + d.owned_off[level]) + (long long)(re - rb - 2) * d.pitch[level];
-        a.up_pitch = d.pitch[level];
-        a.up_flags = reinterpret_cast<const unsigned int *>(c->nb_base[0] + d.flags_off);
+    const int nr = boundary_args(c, level, out, &a);
+    if (nr == 0) {
+        // no neighbour: the whole strip in one level launch, nothing to publish
+        if (part == DWT2_STRIP_BOUNDARY || part == DWT2_STRIP_PUBLISH) return DWT2_OK;
+        return strip_level_launch(p, level, in, c->pitch[level], ll_out, ll_pitch, out, DWT2_STRIP_ALL, s);
     }
-    if (L.ghost_bot) {
-        const dwt2_peer_desc_t &d = c->nb[1];
-        a.dn = reinterpret_cast<const float *>(c->nb_base[1] + d.owned_off[level]);
-        a.dn_pitch = d.pitch[level];
-        a.dn_flags = reinterpret_cast<const unsigned int *>(c->nb_base[1] + d.flags_off);
+    const int qs = L.row_begin / 2, qe = (L.row_end + 1) / 2;
+    const int interior = (qe - (L.ghost_bot ? 1 : 0)) - (qs + (L.ghost_top ? 1 : 0));
+    if (part == DWT2_STRIP_PUBLISH || (part == DWT2_STRIP_INTERIOR && interior <= 0)) {
+        // (an INTERIOR part without interior quad rows still publishes the level)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(1);
+        cfg.blockDim = dim3(1);
+        cfg.stream = s;
+        cudaLaunchAttribute at = pdl_attr();
+        cfg.attrs = &at;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, peer_publish_kernel, c->flags(), (int)level) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(DWT2_ECUDA);
+        }
+        return DWT2_OK;
     }
-    a.flags = c->flags();
-    // output bases as the level kernel computes them (dwt2.cu launch_level)
-    const int Wq = (L.width + 1) / 2;
-    const int hq_local = qe - qs;
-    const int hloc0 = p->row_end - p->row_begin;
-    (void)hloc0;
-    float *mallat = out;                            // level k's subbands start at row 0 of the strip pyramid
-    a.ll = last ? out : ll_out;
-    a.ll_pitch = last ? p->W : ll_pitch;
-    a.hl = mallat + Wq;
-    a.lh = mallat + (long long)hq_local * p->W;
-    a.hh = a.lh + Wq;
-    a.out_pitch = p->W;
-    a.timeout_ns = (long long)c->timeout_ms * 1000000LL;
-    a.W = L.width;
-    a.H = L.global_height;
-    a.rb = L.row_begin;
-    a.re = L.row_end;
-    a.qs = qs;
-    a.n0 = rows[0];
-    a.n1 = nr > 1 ? rows[1] : rows[0];
-    a.level = level;
-    a.last = last ? 1 : 0;
-    a.quiesce = c->mode == DWT2_PEER_RANKS ? 1 : 0;
-
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((Wq + PB_THREADS - 1) / PB_THREADS, nr);
-    cfg.blockDim = dim3(PB_THREADS);
-    cfg.stream = s;
-    cudaLaunchAttribute at = pdl_attr();
-    cfg.attrs = &at;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, peer_boundary_kernel, a) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(DWT2_ECUDA);
+    if (part == DWT2_STRIP_INTERIOR)        // publishes the level at entry, no boundary-role CTAs
+        return strip_level_launch(p, level, in, c->pitch[level], ll_out, ll_pitch, out, DWT2_STRIP_INTERIOR, s, &a, 0);
+    if (part == DWT2_STRIP_BOUNDARY || interior <= 0) {
+        a.nbx = ((L.width + 1) / 2 + PB_THREADS - 1) / PB_THREADS;
+        a.nroles = a.nbx * nr;
+        return launch_boundary(a, nr, s);
     }
-    return DWT2_OK;
+    // ALL: ONE launch -- the level kernel on the interior quad rows plus
+    // boundary-role CTAs (level_kernel_threads() quads each) past its own grid
+    const int threads = level_kernel_threads();
+    a.nbx = ((L.width + 1) / 2 + threads - 1) / threads;
+    a.nroles = a.nbx * nr;
+    return strip_level_launch(p, level, in, c->pitch[level], ll_out, ll_pitch, out, DWT2_STRIP_INTERIOR, s, &a,
+                              a.nroles);
 }
 
 int32_t dwt2_peer_strip_forward(dwt2_peer_strip *c, float *out, dwt2_stream_t stream)
 {
     if (!c || !c->connected || c->mode != DWT2_PEER_RANKS) return fail(DWT2_EINVAL);
-    for (int k = 0; k < c->levels; ++k) {
-        int32_t r = dwt2_peer_strip_level(c, k, DWT2_STRIP_INTERIOR, out, stream);
-        if (r == DWT2_OK) r = dwt2_peer_strip_level(c, k, DWT2_STRIP_BOUNDARY, out, stream);
-        if (r != DWT2_OK) return r;
-    }
-    return DWT2_OK;
+    int32_t r = DWT2_OK;
+    for (int k = 0; k < c->levels && r == DWT2_OK; ++k) r = dwt2_peer_strip_level(c, k, DWT2_STRIP_ALL, out, stream);
+    return r;
 }
 
 int32_t dwt2_peer_strip_status(const dwt2_peer_strip *c)

@@ -307,11 +307,11 @@ def place_pyramid_output(full: np.ndarray, strip_out: np.ndarray, W: int, H: int
 # ---- peer-memory halo (include/dwt2.h "peer strip context") -----------------
 #
 # The same row strips as StripPyramid, with the exchange fused into the level
-# kernels: every rank's level buffers live in one device allocation whose
-# CUDA IPC handle the neighbours map; the BOUNDARY kernel of a level reads the
-# 2 rows above / 1 row below from the neighbour's memory over NVLink once the
-# neighbour's flag says they are final.  Host side, a step is 2 launches per
-# level with no wait, so it can be captured in a CUDA graph.  The descriptors
+# launch: every rank's level buffers live in one device allocation whose CUDA
+# IPC handle the neighbours map; boundary-role CTAs in the level kernel's own
+# launch read the 2 rows above / 1 row below from the neighbour's memory over
+# NVLink once the neighbour's flag says they are final.  Host side, a step is
+# ONE launch per level with no wait, so it can be captured in a CUDA graph.  The descriptors
 # (plain bytes) travel once, through all_gather_object on the process group.
 
 def peer_neighbours(descs: list, rank: int) -> tuple:
@@ -399,13 +399,16 @@ class PeerStripPyramid:
         self.plan.close()
 
 
-def sequential_step(ranks: list, stream=None):
-    """One step of emulated ranks in one stream: for each level, every rank's
-    INTERIOR part (each publishes its level-k ready flag), then every rank's
-    BOUNDARY part -- so no kernel ever waits on a later launch."""
+def sequential_step(ranks: list, stream=None, fused: bool = True):
+    """One step of emulated ranks in one stream, level by level: fused, every
+    rank's PUBLISH launch, then every rank's ALL launch (the one-launch form a
+    rank issues on its own GPU); else every rank's INTERIOR launch (which
+    publishes), then every rank's BOUNDARY launch.  Every flag a launch waits
+    for was published by an earlier launch."""
     from . import dwt2
     for k in range(ranks[0].levels):
-        for r in ranks:
-            r.ctx.level(k, dwt2.DWT2_STRIP_INTERIOR, r.out, stream)
-        for r in ranks:
-            r.ctx.level(k, dwt2.DWT2_STRIP_BOUNDARY, r.out, stream)
+        parts = ((dwt2.DWT2_STRIP_PUBLISH, dwt2.DWT2_STRIP_ALL) if fused
+                 else (dwt2.DWT2_STRIP_INTERIOR, dwt2.DWT2_STRIP_BOUNDARY))
+        for part in parts:
+            for r in ranks:
+                r.ctx.level(k, part, r.out, stream)

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_PKG, "libdwt2.so")      # the in-tree product library (
 DWT2_OK, DWT2_EINVAL, DWT2_ENOMEM, DWT2_ECUDA, DWT2_EUNSUPPORTED, DWT2_ETIMEOUT = 0, -1, -2, -3, -4, -5
 DWT2_PEER_RANKS, DWT2_PEER_SEQUENTIAL = 0, 1
 DWT2_BOUNDARY_SYMMETRIC = 0
-DWT2_STRIP_ALL, DWT2_STRIP_INTERIOR, DWT2_STRIP_BOUNDARY = 0, 1, 2
+DWT2_STRIP_ALL, DWT2_STRIP_INTERIOR, DWT2_STRIP_BOUNDARY, DWT2_STRIP_PUBLISH = 0, 1, 2, 3
 DWT2_WAVELET_CDF53, DWT2_WAVELET_CDF97, DWT2_WAVELET_CDF53_K2, DWT2_WAVELET_LIFTING = 0, 1, 2, 3
 WAVELETS = {"cdf53": 0, "cdf97": 1, "cdf53_k2": 2, "lifting": 3}
 SCHEMES = {"fused": 0, "nonsep_naive": 1, "nonsep_lifting": 2, "nonsep_adapted": 3, "sep_conv": 4,

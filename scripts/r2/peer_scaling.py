@@ -31,6 +31,7 @@ for name, W, H, L in [("config 3", 16384, 16384, 1), ("config 4", 8192, 8192, 8)
             r.connect_local(ranks)
             r.strip.copy_(x[r.r0:r.r1])
         t_peer = time_calls(lambda q: D.sequential_step(ranks), [(None,)], 10)
+        t_split = time_calls(lambda q: D.sequential_step(ranks, fused=False), [(None,)], 10)
         torch.cuda.synchronize()
         h0 = time.perf_counter()
         for _ in range(20):
@@ -55,7 +56,8 @@ for name, W, H, L in [("config 3", 16384, 16384, 1), ("config 4", 8192, 8192, 8)
         for plan in plans:
             plan.close()
         del pyrs
-        print(f"{name}: G={G} peer {t_peer:7.1f} us / step of all ranks ({t_peer / G:6.1f} per rank, "
-              f"T1/sum {t1 / t_peer:.2f}), host enqueue {(h1 - h0) / 20 * 1e6 / G:5.1f} us per rank-step; "
+        print(f"{name}: G={G} peer fused {t_peer:7.1f} us / step of all ranks ({t_peer / G:6.1f} per rank, "
+              f"T1/sum {t1 / t_peer:.2f}); peer split {t_split:7.1f} ({t_split / G:6.1f} per rank); "
+              f"host enqueue {(h1 - h0) / 20 * 1e6 / G:5.1f} us per rank-step; "
               f"nccl-stub {t_stub:7.1f} us ({t_stub / G:6.1f} per rank, T1/sum {t1 / t_stub:.2f}); status {set(st)}",
               flush=True)

@@ -3,10 +3,12 @@
 point of PAPER.md L94-98).
 
 Every rank's context lives on cuda:0 and the ranks run in ONE stream in the
-DWT2_PEER_SEQUENTIAL order (for each level: all INTERIOR parts, which publish
-the level's ready flag, then all BOUNDARY parts, which acquire the
-neighbours' flags and read their rows), so no kernel ever waits for a later
-launch.  The placed strip pyramids must equal the single-GPU dwt2_forward bit
+DWT2_PEER_SEQUENTIAL order (per level: every rank's PUBLISH launch, then
+every rank's fused launch; or every rank's INTERIOR launch, which publishes,
+then every rank's BOUNDARY launch), so every flag a launch waits for was
+published by an earlier launch.  Both level forms are covered: the fused one
+(DWT2_STRIP_ALL: the level kernel plus boundary-role CTAs in ONE launch -- the
+step's form) and the split one.  The placed strip pyramids must equal the single-GPU dwt2_forward bit
 for bit and the oracle (ii) bit for bit (fp64 register arithmetic, the
 per-level fp32 rounding of oracle (ii)).
 """
@@ -60,17 +62,18 @@ def close(ranks):
 @pytest.mark.parametrize("W,H,G,L", [
     (64, 64, 2, 1), (64, 64, 2, 3), (130, 97, 3, 2), (300, 212, 2, 1), (1000, 1030, 4, 4), (333, 2049, 8, 3),
     (4096, 4096, 8, 5), (1537, 1025, 3, 6), (257, 512, 2, 8), (8, 64, 4, 1), (5, 40, 5, 2), (1030, 16, 4, 2)])
-def test_peer_strips_equal_single_gpu_and_oracle(W, H, G, L):
+@pytest.mark.parametrize("fused", [True, False])
+def test_peer_strips_equal_single_gpu_and_oracle(W, H, G, L, fused):
     x = workloads.uniform_real(W, H, 3 * W + H + L)
     ranks = make_ranks(W, H, G, L)
     fill(ranks, x)
-    D.sequential_step(ranks)
+    D.sequential_step(ranks, fused=fused)
     got = gather(ranks, W, H, L)
     close(ranks)
     assert not np.isnan(got).any()
     np.testing.assert_array_equal(got, single_gpu(x, L))
     x64 = x.astype(np.float64)
-    what = f"peer strips {W}x{H} G{G} L{L}"
+    what = f"peer strips {W}x{H} G{G} L{L} fused={fused}"
     compare(got, None, oracle.forward(x64, L, round_f32=True), True, what)       # bit-exact vs oracle (ii)
     compare(got, oracle.forward(x64, L), None, False, what)                      # within 1e-4 of oracle (i)
 
@@ -80,12 +83,13 @@ def test_peer_strips_two_row_strips():
     reads 2 rows above AND 1 row below from the neighbours)."""
     for (W, H, G, L) in [(48, 32, 8, 1), (48, 16, 8, 1), (40, 64, 8, 2)]:
         x = workloads.uniform_int(W, H, W + H)
-        ranks = make_ranks(W, H, G, L)
-        fill(ranks, x)
-        D.sequential_step(ranks)
-        got = gather(ranks, W, H, L)
-        close(ranks)
-        np.testing.assert_array_equal(got, oracle.forward(x.astype(np.float64), L, round_f32=True).astype(np.float32))
+        for fused in (True, False):
+            ranks = make_ranks(W, H, G, L)
+            fill(ranks, x)
+            D.sequential_step(ranks, fused=fused)
+            got = gather(ranks, W, H, L)
+            close(ranks)
+            np.testing.assert_array_equal(got, oracle.forward(x.astype(np.float64), L, round_f32=True).astype(np.float32))
 
 
 def test_peer_strips_config3_g8_and_config4_g8():
@@ -106,10 +110,10 @@ def test_peer_strips_repeated_steps_new_inputs():
     correct (stale rows or flags of an earlier step would show)."""
     W, H, G, L = 520, 384, 4, 3
     ranks = make_ranks(W, H, G, L)
-    for s in range(4):
+    for s in range(6):
         x = workloads.uniform_real(W, H, 100 + s)
         fill(ranks, x)
-        D.sequential_step(ranks)
+        D.sequential_step(ranks, fused=s % 2 == 0)
         np.testing.assert_array_equal(gather(ranks, W, H, L), single_gpu(x, L))
     close(ranks)
 
@@ -158,8 +162,7 @@ def test_peer_wait_times_out_instead_of_hanging():
     ranks = make_ranks(W, H, G, L, timeout_ms=50)
     fill(ranks, workloads.uniform_int(W, H, 1))
     r0 = ranks[0]
-    r0.ctx.level(0, dwt2.DWT2_STRIP_INTERIOR, r0.out)      # rank 1's INTERIOR never runs
-    r0.ctx.level(0, dwt2.DWT2_STRIP_BOUNDARY, r0.out)
+    r0.ctx.level(0, dwt2.DWT2_STRIP_ALL, r0.out)            # rank 1 never publishes its level 0
     torch.cuda.synchronize()
     assert r0.status() == dwt2.DWT2_ETIMEOUT
     assert ranks[1].status() == dwt2.DWT2_OK
