@@ -259,17 +259,28 @@ static __device__ __noinline__ void peer_boundary_role(const PeerBoundaryArgs &a
     const int Wq = (W + 1) >> 1, Wh = W >> 1, Hh = H >> 1;
     const int m0 = bx * nt;
     const int c0 = 2 * m0 - 2;
+    // every load of the thread in flight at once (one memory round trip; a
+    // load / smem-store loop paid one round trip per element: ~10 us per CTA)
+    float v[5][3];                        // cols <= 3 nt for nt >= 4
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
         const int y = peer_wss2(2 * n - 2 + j, H);
         const float *row = y < a.rb ? a.up + (long long)(y - (a.rb - 2)) * a.up_pitch
                          : y >= a.re ? a.dn + (long long)(y - a.re) * a.dn_pitch
                                      : a.own + (long long)(y - a.rb) * a.own_pitch;
-        for (int i = threadIdx.x; i < cols; i += nt) {
-            const int x = c0 + i;
-            if (x <= W + 1) tile[j * cols + i] = __ldcg(row + peer_wss2(x, W));
+#pragma unroll
+        for (int it = 0; it < 3; ++it) {
+            const int i = threadIdx.x + it * nt, x = c0 + i;
+            v[j][it] = (i < cols && x <= W + 1) ? __ldcg(row + peer_wss2(x, W)) : 0.f;
         }
     }
+#pragma unroll
+    for (int j = 0; j < 5; ++j)
+#pragma unroll
+        for (int it = 0; it < 3; ++it) {
+            const int i = threadIdx.x + it * nt;
+            if (i < cols) tile[j * cols + i] = v[j][it];
+        }
     __syncthreads();
     const int m = m0 + threadIdx.x;
     if (m < Wq) {
