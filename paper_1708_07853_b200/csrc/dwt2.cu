@@ -1637,6 +1637,19 @@ LaunchIO level_io(const dwt2_plan *p, const float *in, float *out, int count, lo
     return io;
 }
 
+// Levels that run on the small-level kernel (tail.cu launch_small_level) when
+// they are not in the tail launch.  Measured (scripts/r2/small_probe.py, graph
+// of 20 calls): a single 512^2 level 4.05 -> 3.74 us (2^16 quads), 1024^2
+// 5.34 -> 5.87 us (slower from a cold input); inside a pyramid, where a
+// level's input is the LL just written (in L2), the 1024^2 level pays too:
+// config 4 139.3 -> 137.7 us, 4b 150.7 -> 148.9 with levels of <= 2^18 quads.
+bool small_level(const dwt2_plan *p, int k, int count)
+{
+    static const long long small_first = tuning_int("DWT2_SMALL_QUADS", 1 << 16, 0, 1 << 30);
+    static const long long small_ll = tuning_int("DWT2_SMALL_QUADS_LL", 1 << 18, 0, 1 << 30);
+    return (long long)p->geom[k].Wq * p->geom[k].Hq * count <= (k == 0 ? small_first : small_ll);
+}
+
 // Forward of levels [first, last] for `count` images.  Level 1 reads `in`.
 // Level-1 quad rows may be restricted to [q1a, q1b) (host pipelining).  The
 // small last levels (tail_start) run as one tail launch, the others one
@@ -1659,6 +1672,15 @@ int32_t run_levels(const dwt2_plan *p, const float *in, float *out, int count, l
         if (k == 0) {
             qa = q1a;
             qb = q1b;
+        }
+        // small levels (whole level, product arithmetic): the shared-memory
+        // tiled pointwise kernel (tail.cu) instead of the row-walking level kernel
+        if (ar == AR_GROUPED && qa == 0 && qb == g.Hq && small_level(p, k, count)) {
+            const TailLevelIO lv{io.in, io.in_pitch, io.in_img_stride, io.ll, io.ll_pitch, io.ll_img_stride,
+                                 io.out, io.out_pitch, io.out_img_stride, g.W, g.H};
+            int32_t r = launch_small_level(lv, count, s);
+            if (r != DWT2_OK) return r;
+            continue;
         }
         int32_t r = launch_level(p, k, g.W, g.H, io, qa, qb, 0, 0, s, 0, ar);
         if (r != DWT2_OK) return r;
@@ -2078,10 +2100,16 @@ int32_t dwt2_plan_info(const dwt2_plan *p, dwt2_plan_info_t *info)
     }
     int tma = 0;
     long long bytes = 0;
+    const int t0 = p->strip ? p->levels
+                            : (p->wavelet == DWT2_WAVELET_CDF53 ? tail_start(p, p->max_count, 0, p->levels - 1)
+                                                                 : k2_tail_start(p, p->max_count));
     for (int k = 0; k < p->levels; ++k) {
         const LevelGeom &g = p->geom[k];
+        // level kernel levels (not the tail launch, not the small-level kernel);
         // level 1 reads the caller's buffer: TMA iff its rows are 16-byte aligned
-        if (k > 0 || (p->W % 4) == 0) ++tma;
+        const bool level_kernel = k < t0 && (p->strip || p->wavelet != DWT2_WAVELET_CDF53 ||
+                                             !small_level(p, k, p->max_count));
+        if (level_kernel && p->wavelet == DWT2_WAVELET_CDF53 && (k > 0 || (p->W % 4) == 0)) ++tma;
         long long rows = g.H;
         if (p->strip) {
             dwt2_strip_level_t L;

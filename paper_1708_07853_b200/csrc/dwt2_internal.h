@@ -361,6 +361,8 @@ TailFilter tail_filter_from_lifting(double c0, double c1, double c2, double c3, 
 int tail_start_levels(const dwt2_plan *p, int count, int first, int last, long long max_quads);
 int32_t launch_tail_levels(const dwt2_plan *p, const TailLevelIO *lv, int n, int count, const TailFilter &f,
                            cudaStream_t stream);
+// one small CDF 5/3 level in one launch of shared-memory-tiled pointwise CTAs (tail.cu)
+int32_t launch_small_level(const TailLevelIO &lv, int count, cudaStream_t stream);
 
 // true if ptr is device (or managed) memory of the plan's device
 bool on_plan_device(const dwt2_plan *p, const void *ptr);

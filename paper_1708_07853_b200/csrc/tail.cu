@@ -172,6 +172,69 @@ __global__ void __launch_bounds__(TAIL_THREADS) dwt_tail_kernel(const __grid_con
     }
 }
 
+// ---- small single levels: one launch, one CTA per 32 x 8 quad block ------
+//
+// A level of at most a few MB (config 1: 512^2) is latency-bound on the level
+// kernel, whose warps walk their tiles row by row through a TMA ring (a serial
+// fp64 chain of ~3 us per 8-row stage).  Here a CTA loads the 19 x 67 input
+// pixels its 32 x 8 quads depend on (rows 2 n0 - 2 .. 2 n0 + 16, columns
+// 2 m0 - 2 .. 2 m0 + 64, whole-sample symmetric at the image edges) into
+// shared memory in ONE round of independent coalesced loads, and every thread
+// evaluates one quad pointwise with the exact 5 x 5 analysis filters of the
+// radius-2 tail path (bit for bit the level kernel's values).
+constexpr int SQX = 32, SQY = 8;                         // quads per CTA
+constexpr int STR = 2 * SQY + 3, STC = 2 * SQX + 3;      // staged rows / columns
+constexpr int SN = (STR * STC + 255) / 256;              // staged floats per thread
+
+__global__ void __launch_bounds__(256) dwt53_small_kernel(const __grid_constant__ TailLevelIO L, int nbx)
+{
+    __shared__ float t[STR][STC + 1];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int W = L.W, H = L.H;
+    const int Wq = (W + 1) >> 1, Hq = (H + 1) >> 1, Wh = W >> 1, Hh = H >> 1;
+    const int bx = blockIdx.x % nbx, by = blockIdx.x / nbx, img = blockIdx.y;
+    const int m0 = bx * SQX, n0 = by * SQY;
+    const float *x = L.in + img * L.in_img;
+    float v[SN];
+#pragma unroll
+    for (int k = 0; k < SN; ++k) {                       // every load in flight at once
+        const int i = threadIdx.x + 256 * k;
+        const int r = i / STC, c = i - (i / STC) * STC;
+        const int yy = 2 * n0 - 2 + r, xx = 2 * m0 - 2 + c;
+        v[k] = (i < STR * STC && yy <= H + 1 && xx <= W + 1)
+                   ? __ldg(x + (long long)wss2(yy, H) * L.in_pitch + wss2(xx, W)) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < SN; ++k) {
+        const int i = threadIdx.x + 256 * k;
+        if (i < STR * STC) t[i / STC][i - (i / STC) * STC] = v[k];
+    }
+    __syncthreads();
+    const int tx = threadIdx.x & (SQX - 1), ty = threadIdx.x / SQX;
+    const int m = m0 + tx, n = n0 + ty;
+    if (m >= Wq || n >= Hq) return;
+    double lo[5], hi[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const float *w = &t[2 * ty + j][2 * tx];
+        const double v0 = w[0], v1 = w[1], v2 = w[2], v3 = w[3], v4 = w[4];
+        lo[j] = fma(0.75, v2, fma(0.25, v1 + v3, -0.125 * (v0 + v4)));
+        hi[j] = fma(-0.5, v2 + v4, v3);
+    }
+    const double ll = fma(0.75, lo[2], fma(0.25, lo[1] + lo[3], -0.125 * (lo[0] + lo[4])));
+    const double lh = fma(-0.5, lo[2] + lo[4], lo[3]);
+    const double hl = fma(0.75, hi[2], fma(0.25, hi[1] + hi[3], -0.125 * (hi[0] + hi[4])));
+    const double hh = fma(-0.5, hi[2] + hi[4], hi[3]);
+    L.ll[img * L.ll_img + (long long)n * L.ll_pitch + m] = (float)ll;
+    float *o = L.out + img * L.out_img;
+    if (m < Wh) o[(long long)n * L.out_pitch + Wq + m] = (float)hl;
+    if (n < Hh) {
+        o[(long long)(Hq + n) * L.out_pitch + m] = (float)lh;
+        if (m < Wh) o[(long long)(Hq + n) * L.out_pitch + Wq + m] = (float)hh;
+    }
+}
+
 template <int R>
 int tail_resident()
 {
@@ -228,6 +291,27 @@ TailFilter tail_filter_from_lifting(double c0, double c1, double c2, double c3, 
     f.sd = 1.0;
     f.shh = K * K;
     return f;
+}
+
+int32_t launch_small_level(const TailLevelIO &lv, int count, cudaStream_t stream)
+{
+    const int Wq = (lv.W + 1) / 2, Hq = (lv.H + 1) / 2;
+    const int nbx = (Wq + SQX - 1) / SQX, nby = (Hq + SQY - 1) / SQY;
+    if ((long long)nbx * nby >= (1LL << 31) || count > 65535) return fail(DWT2_EINVAL);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nbx * nby, count);
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, dwt53_small_kernel, lv, nbx) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DWT2_ECUDA);
+    }
+    return DWT2_OK;
 }
 
 int tail_start_levels(const dwt2_plan *p, int count, int first, int last, long long max_quads)
