@@ -296,7 +296,8 @@ class OursRunner:
             r0, r1 = self.ex.r0, self.ex.r1
             self.ex.strip.copy_(torch.from_numpy(np.ascontiguousarray(img[r0:r1])))
             self.out = self.ex.out
-            self.launches = cfg.levels * (1 if (self.overlap_off and self.exchange == "nccl") else 2)
+            # peer: one launch per level (interior tiles + boundary-role CTAs); nccl: interior + boundary
+            self.launches = cfg.levels * (1 if (self.overlap_off or self.exchange == "peer") else 2)
             self.algo_bytes = sum(BYTES_PER_PX * w * (re - rb) for (w, h, rb, re, gt, gb) in self.ex.geom)
             self.level1_bytes = BYTES_PER_PX * g.width * (r1 - r0)
             self.pixels = g.width * (r1 - r0)
