@@ -288,9 +288,21 @@ class OursRunner:
             self.sha.update(img.tobytes())
             if self.exchange == "peer":
                 self.ex = D.PeerStripPyramid(g.width, g.height, rank, world, cfg.levels, device=device)
-                self.ex.connect()              # all_gather of the CUDA IPC descriptors (once)
+                try:
+                    self.ex.connect()          # all_gather of the CUDA IPC descriptors (once)
+                    ok = 1
+                except dwt2.DWT2Error as e:   # e.g. no CUDA IPC between the processes
+                    ok, self.peer_error = 0, str(e)
+                import torch.distributed as dist
+                flag = torch.tensor([ok], device=device)
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+                if not int(flag.item()):
+                    # every rank switches to the NCCL exchange together (a GPU path too)
+                    self.ex.close()
+                    OursRunner.exchange = "nccl"
+                    self.exchange_note = "peer mapping failed (%s): NCCL exchange" % getattr(self, "peer_error", "another rank")
                 self.splan = None
-            else:
+            if self.exchange == "nccl":
                 self.ex = D.StripPyramid(g.width, g.height, rank, world, cfg.levels, device=device)
                 self.splan = dwt2.StripPlan(g.width, g.height, self.ex.r0, self.ex.r1, cfg.levels)
             r0, r1 = self.ex.r0, self.ex.r1
@@ -902,7 +914,7 @@ def main():
         runner.step()
     torch.cuda.synchronize()
     graph = None
-    if not args.no_graph and (runner.mode != "strip" or args.exchange == "peer"):
+    if not args.no_graph and (runner.mode != "strip" or OursRunner.exchange == "peer"):
         # the K timed steps as ONE CUDA graph (the level kernels keep their
         # programmatic dependent-launch edges): no host launch gaps, and the
         # NVML sampler thread cannot gate the GPU
@@ -1004,7 +1016,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(args, cfg, world),
+            "config": dict(config_dict(args, cfg, world),
+                           **({"exchange_note": runner.exchange_note} if getattr(runner, "exchange_note", None) else {})),
             "gate": gate_res,
             "step_stats": stats,
             "warm_l2": warm,
