@@ -381,6 +381,13 @@ class PeerStripPyramid:
         above, below = peer_neighbours(gather_descriptors(self.export(), group), self.rank)
         self.ctx.connect(above, below, dwt2.DWT2_PEER_RANKS)
 
+    def connect_descriptors(self, descs: list, mode=None):
+        """Connect from the descriptor bytes of every rank (rank order), however
+        they were gathered (a process group, a pipe between processes)."""
+        from . import dwt2
+        above, below = peer_neighbours(descs, self.rank)
+        self.ctx.connect(above, below, dwt2.DWT2_PEER_RANKS if mode is None else mode)
+
     def connect_local(self, ranks: list, mode=None):
         """Ranks of one process (this object is ranks[self.rank])."""
         from . import dwt2

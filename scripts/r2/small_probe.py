@@ -15,12 +15,17 @@ from paper_1708_07853_b200 import _build, dwt2  # noqa: E402
 mode = sys.argv[1] if len(sys.argv) > 1 else "product"
 if mode != "product":
     os.environ["DWT2_SMALL_QUADS"] = mode
+    os.environ["DWT2_SMALL_QUADS_LL"] = os.environ.get("LLQ", "262144")
     dwt2.use_variant(_build.build_variant("tuning", {"DWT2_TUNING": 1}))
 from _timing import time_calls  # noqa: E402
 from paper_1708_07853_b200 import workloads  # noqa: E402
 
-for name, W, H, L in [("config 1", 512, 512, 1), ("256^2", 256, 256, 1), ("1024^2", 1024, 1024, 1),
-                      ("config 4", 8192, 8192, 8), ("config 4b", 8193, 8193, 8)]:
+CASES = [("config 1", 512, 512, 1), ("256^2", 256, 256, 1), ("1024^2", 1024, 1024, 1),
+         ("config 4", 8192, 8192, 8), ("config 4b", 8193, 8193, 8)]
+if len(sys.argv) > 2 and sys.argv[2] == "mid":
+    CASES = [("2048^2", 2048, 2048, 1), ("config 2", 4096, 4096, 1), ("16384x2048", 16384, 2048, 1),
+             ("8192^2", 8192, 8192, 1), ("config 4", 8192, 8192, 8)]
+for name, W, H, L in CASES:
     K = 20
     npairs = K if W * H * 8 < 2 * 126e6 else 1
     x = torch.from_numpy(workloads.uniform_int(W, H, 1)).cuda()
