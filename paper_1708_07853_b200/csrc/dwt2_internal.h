@@ -363,6 +363,8 @@ int32_t launch_tail_levels(const dwt2_plan *p, const TailLevelIO *lv, int n, int
                            cudaStream_t stream);
 // one small CDF 5/3 level in one launch of shared-memory-tiled pointwise CTAs (tail.cu)
 int32_t launch_small_level(const TailLevelIO &lv, int count, cudaStream_t stream);
+// one small level of a K <= 2 lifting wavelet (radius-4 filters f) in one launch (tail.cu)
+int32_t launch_small_level_r4(const TailLevelIO &lv, int count, const TailFilter &f, cudaStream_t stream);
 
 // true if ptr is device (or managed) memory of the plan's device
 bool on_plan_device(const dwt2_plan *p, const void *ptr);

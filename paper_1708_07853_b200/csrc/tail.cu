@@ -235,6 +235,94 @@ __global__ void __launch_bounds__(256) dwt53_small_kernel(const __grid_constant_
     }
 }
 
+// ---- small single levels of a K <= 2 lifting wavelet (radius-4 filters) ---
+//
+// The K = 2 level kernel walks a tile row by row through four lifting steps and
+// four warm-up rows; a level of a few MB is a chain of such walks.  Here a CTA
+// of 256 threads owns 32 x 8 quads: it stages the 23 x 71 input pixels they
+// depend on (mirrored) in shared memory in one round of loads, runs the row
+// pass once per staged row and quad column (the 9 low taps at column 2m, the 7
+// high taps at 2m + 1, in fp64, into shared memory), then every thread runs the
+// column pass of its quad and the 2-D scaling -- the tail kernel's radius-4
+// evaluation, term for term, with each row pass shared by the quads above and
+// below it.  Measured (scripts/r2/k2small_probe.py): a 1024^2 9/7 level 9.53 ->
+// 8.72 us, the 9/7 config-4 pyramid 175.6 -> 174.4 us; from 2048^2 up it loses
+// (15.2 -> 29.0 us: shared-memory and fp64 issue bound; staging the tile as fp64
+// to save the conversions was slower still, 43 us: 16-byte-strided reads), so
+// levels of <= 2^18 quads only.
+constexpr int R4X = 32, R4Y = 8;
+constexpr int R4R = 2 * R4Y + 7, R4C = 2 * R4X + 7;      // staged rows / columns
+constexpr int R4N = (R4R * R4C + 255) / 256;
+
+struct Small4Args {
+    TailLevelIO L;
+    double h[9], g[7];
+    double sll, sd, shh;
+    int nbx;
+};
+
+__global__ void __launch_bounds__(256) dwt_small4_kernel(const __grid_constant__ Small4Args A)
+{
+    __shared__ float t[R4R][R4C + 1];
+    __shared__ double lo[R4R][R4X], hi[R4R][R4X];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const TailLevelIO &L = A.L;
+    const int W = L.W, H = L.H;
+    const int Wq = (W + 1) >> 1, Hq = (H + 1) >> 1, Wh = W >> 1, Hh = H >> 1;
+    const int bx = blockIdx.x % A.nbx, by = blockIdx.x / A.nbx, img = blockIdx.y;
+    const int m0 = bx * R4X, n0 = by * R4Y;
+    const float *x = L.in + img * L.in_img;
+    float v[R4N];
+#pragma unroll
+    for (int k = 0; k < R4N; ++k) {                      // every load in flight at once
+        const int i = threadIdx.x + 256 * k;
+        const int r = i / R4C, c = i - (i / R4C) * R4C;
+        const int yy = 2 * n0 - 4 + r, xx = 2 * m0 - 4 + c;
+        v[k] = (i < R4R * R4C && yy < H + 4 && xx < W + 4)
+                   ? __ldg(x + (long long)wss_fast(yy, H) * L.in_pitch + wss_fast(xx, W)) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < R4N; ++k) {
+        const int i = threadIdx.x + 256 * k;
+        if (i < R4R * R4C) t[i / R4C][i - (i / R4C) * R4C] = v[k];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < R4R * R4X; i += 256) {    // row passes
+        const int r = i / R4X, q = i - (i / R4X) * R4X;
+        const float *w = &t[r][2 * q];
+        double s = 0.0, u = 0.0;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) s = fma(A.h[j], (double)w[j], s);
+#pragma unroll
+        for (int j = 0; j < 7; ++j) u = fma(A.g[j], (double)w[j + 2], u);
+        lo[r][q] = s;
+        hi[r][q] = u;
+    }
+    __syncthreads();
+    const int tx = threadIdx.x & (R4X - 1), ty = threadIdx.x / R4X;
+    const int m = m0 + tx, n = n0 + ty;
+    if (m >= Wq || n >= Hq) return;
+    double ll = 0.0, hl = 0.0, lh = 0.0, hh = 0.0;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        ll = fma(A.h[j], lo[2 * ty + j][tx], ll);
+        hl = fma(A.h[j], hi[2 * ty + j][tx], hl);
+    }
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {
+        lh = fma(A.g[j], lo[2 * ty + j + 2][tx], lh);
+        hh = fma(A.g[j], hi[2 * ty + j + 2][tx], hh);
+    }
+    L.ll[img * L.ll_img + (long long)n * L.ll_pitch + m] = (float)(ll * A.sll);
+    float *o = L.out + img * L.out_img;
+    if (m < Wh) o[(long long)n * L.out_pitch + Wq + m] = (float)(hl * A.sd);
+    if (n < Hh) {
+        o[(long long)(Hq + n) * L.out_pitch + m] = (float)(lh * A.sd);
+        if (m < Wh) o[(long long)(Hq + n) * L.out_pitch + Wq + m] = (float)(hh * A.shh);
+    }
+}
+
 template <int R>
 int tail_resident()
 {
@@ -308,6 +396,37 @@ int32_t launch_small_level(const TailLevelIO &lv, int count, cudaStream_t stream
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, dwt53_small_kernel, lv, nbx) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DWT2_ECUDA);
+    }
+    return DWT2_OK;
+}
+
+int32_t launch_small_level_r4(const TailLevelIO &lv, int count, const TailFilter &f, cudaStream_t stream)
+{
+    if (f.radius != 4) return fail(DWT2_EINVAL);
+    const int Wq = (lv.W + 1) / 2, Hq = (lv.H + 1) / 2;
+    Small4Args A;
+    memset(&A, 0, sizeof(A));
+    A.L = lv;
+    memcpy(A.h, f.h, sizeof(A.h));
+    memcpy(A.g, f.g, sizeof(A.g));
+    A.sll = f.sll;
+    A.sd = f.sd;
+    A.shh = f.shh;
+    A.nbx = (Wq + R4X - 1) / R4X;
+    const int nby = (Hq + R4Y - 1) / R4Y;
+    if ((long long)A.nbx * nby >= (1LL << 31) || count > 65535) return fail(DWT2_EINVAL);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(A.nbx * nby, count);
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, dwt_small4_kernel, A) != cudaSuccess) {
         cudaGetLastError();
         return fail(DWT2_ECUDA);
     }
