@@ -747,7 +747,7 @@ __device__ __forceinline__ void storeq(float *p, const float (&x)[QPL], int n, b
 // streams tiles from the work queue through its own TMA ring (producer and
 // consumer in one warp, prefetching across tile boundaries).
 // ---------------------------------------------------------------------------
-template <bool TMA, bool VEC, int AR, int GG, int NS = S>
+template <bool TMA, bool VEC, int AR, int GG, int NS = S, bool PEER = false>
 __global__ void __launch_bounds__(THREADS, NS == 2 ? DWT2_MINB : 3)
 dwt53_level_kernel(const __grid_constant__ LevelArgs a)
 {
@@ -781,6 +781,9 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
     // complete, so this level's input rows are final -- tell the neighbours;
     // in a fused launch the CTAs past the level's own grid compute the strip's
     // boundary quad rows from the neighbours' memory
+    // (a separate instantiation: the hooks cost the other launches measurably --
+    // config 5's 2048^2 x 256 batch 1737 -> 1808 us with them compiled in)
+    if constexpr (PEER) {
     if (a.peer && blockIdx.x == 0 && threadIdx.x == 0) peer_publish(a.pb.flags, a.pb.level);
     if (a.pb_ctas > 0 && int(blockIdx.x) >= int(gridDim.x) - a.pb_ctas) {
         const int c = int(blockIdx.x) - (int(gridDim.x) - a.pb_ctas);
@@ -788,6 +791,7 @@ dwt53_level_kernel(const __grid_constant__ LevelArgs a)
         __syncthreads();
         if (threadIdx.x == 0) peer_exit(a.pb);
         return;
+    }
     }
 #ifdef DWT2_PROF
     if (threadIdx.x == 0 && blockIdx.x < 4096) {
@@ -1116,6 +1120,15 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode()
 typedef void (*KernelFn)(LevelArgs);
 
 // the 3-stage product kernel of large levels (3-D TMA loader, grouped arithmetic)
+// peer strip launches (peer.cu; their buffers always take the 3-D TMA loader)
+KernelFn kernel_peer(bool large, bool vec)
+{
+    if (large)
+        return vec ? dwt53_level_kernel<true, true, AR_GROUPED, 1, S_LARGE, true>
+                   : dwt53_level_kernel<true, false, AR_GROUPED, 1, S_LARGE, true>;
+    return vec ? dwt53_level_kernel<true, true, AR_GROUPED, 1, S, true> : dwt53_level_kernel<true, false, AR_GROUPED, 1, S, true>;
+}
+
 KernelFn kernel_large(bool vec)
 {
     return vec ? dwt53_level_kernel<true, true, AR_GROUPED, 1, S_LARGE> : dwt53_level_kernel<true, false, AR_GROUPED, 1, S_LARGE>;
@@ -1381,7 +1394,12 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, s3 ? kernel_large(vec) : kernel_for(tma || grp, vec, ar, grp ? 1 << glog : 1), a);
+    KernelFn fn = s3 ? kernel_large(vec) : kernel_for(tma || grp, vec, ar, grp ? 1 << glog : 1);
+    if (io.peer) {
+        if (!tma || ar != AR_GROUPED) return fail(DWT2_EINVAL);        // peer.cu buffers are TMA-aligned
+        fn = kernel_peer(s3, vec);
+    }
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fn, a);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(DWT2_ECUDA);
@@ -1436,7 +1454,11 @@ int32_t configure_kernels(int *max_ctas)
         }
         for (int v = 0; v < 2; ++v)
             if (cudaFuncSetAttribute(kernel_large(v == 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(Ring<true, S_LARGE>::SMEM)) != cudaSuccess) {
+                                     int(Ring<true, S_LARGE>::SMEM)) != cudaSuccess ||
+                cudaFuncSetAttribute(kernel_peer(true, v == 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(Ring<true, S_LARGE>::SMEM)) != cudaSuccess ||
+                cudaFuncSetAttribute(kernel_peer(false, v == 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(Ring<true>::SMEM)) != cudaSuccess) {
                 status = DWT2_ECUDA;
                 return;
             }

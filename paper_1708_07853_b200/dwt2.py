@@ -117,8 +117,13 @@ def lib() -> ctypes.CDLL:
             raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
                                "(nvcc for sm_100a); there is no CPU fallback")
         l = ctypes.CDLL(LIB_PATH)
+        product = os.path.abspath(LIB_PATH) == os.path.join(_PKG, "libdwt2.so")
         for name, (res, args) in SIGNATURES.items():
-            fn = getattr(l, name)
+            fn = getattr(l, name, None)
+            if fn is None:
+                if product:
+                    raise RuntimeError(f"{LIB_PATH} does not export {name}: rebuild (__graft_entry__.build())")
+                continue                  # an older measurement build (use_variant) without this entry point
             fn.restype = res
             fn.argtypes = args
         _lib = l
