@@ -32,6 +32,12 @@ for name, W, H, L in [("config 3", 16384, 16384, 1), ("config 4", 8192, 8192, 8)
             r.strip.copy_(x[r.r0:r.r1])
         t_peer = time_calls(lambda q: D.sequential_step(ranks), [(None,)], 10)
         t_split = time_calls(lambda q: D.sequential_step(ranks, fused=False), [(None,)], 10)
+
+        def publish_only(q):               # the emulation's PUBLISH launches alone (a rank on its own GPU has none)
+            for k in range(L):
+                for r in ranks:
+                    r.ctx.level(k, dwt2.DWT2_STRIP_PUBLISH, r.out)
+        t_pub = time_calls(publish_only, [(None,)], 10)
         torch.cuda.synchronize()
         h0 = time.perf_counter()
         for _ in range(20):
@@ -57,6 +63,7 @@ for name, W, H, L in [("config 3", 16384, 16384, 1), ("config 4", 8192, 8192, 8)
             plan.close()
         del pyrs
         print(f"{name}: G={G} peer fused {t_peer:7.1f} us / step of all ranks ({t_peer / G:6.1f} per rank, "
+              f"{(t_peer - t_pub) / G:6.1f} without the emulation's {G * L} PUBLISH launches [{t_pub:5.1f} us], "
               f"T1/sum {t1 / t_peer:.2f}); peer split {t_split:7.1f} ({t_split / G:6.1f} per rank); "
               f"host enqueue {(h1 - h0) / 20 * 1e6 / G:5.1f} us per rank-step; "
               f"nccl-stub {t_stub:7.1f} us ({t_stub / G:6.1f} per rank, T1/sum {t1 / t_stub:.2f}); status {set(st)}",
