@@ -200,18 +200,19 @@ int32_t dwt2_forward_batched(const dwt2_plan *plan, const float *in, float *out,
 int32_t dwt2_forward_strip(const dwt2_plan *plan, const float *in, float *out, int32_t part,
                            dwt2_stream_t stream);
 
-/* ---- Row strips with the halo exchange fused into the boundary kernels --
+/* ---- Row strips with the halo exchange fused into the level launch --------
  *
  * The paper's synchronisation point between cores is the exchange of the
  * samples a step needs from its neighbours (section 3; the
  * row bands of SPEC.md L313-318).  A peer strip context replaces the message
  * exchange of dwt2_forward_strip_level (ghost rows copied by NCCL before the
- * BOUNDARY launch) with device-side PEER READS: the boundary kernel of level
- * k waits on the neighbour's level-k ready flag and loads the 2 rows above /
- * 1 row below straight from the neighbour's buffer (NVLink peer memory
- * mapped through CUDA IPC, or the same device for ranks emulated in one
- * process).  No host call sits between the levels, so a whole step is a
- * stream-ordered sequence of 2 launches per level (CUDA-graph capturable).
+ * BOUNDARY launch) with device-side PEER READS: boundary-role CTAs, appended
+ * to the level kernel's own launch, wait on the neighbour's level-k ready
+ * flag and load the 2 rows above / 1 row below straight from the
+ * neighbour's buffer (NVLink peer memory mapped through CUDA IPC, or the same
+ * device for ranks emulated in one process) while the interior tiles run.
+ * No host call sits between the levels, so a whole step is a stream-ordered
+ * sequence of ONE launch per level (CUDA-graph capturable).
  *
  * Synchronisation (flags in the context's own device memory, epochs counted
  * on the device): the first launch of level k publishes ready[k] = e once it
