@@ -361,6 +361,27 @@ TailFilter tail_filter_from_lifting(double c0, double c1, double c2, double c3, 
 int tail_start_levels(const dwt2_plan *p, int count, int first, int last, long long max_quads);
 int32_t launch_tail_levels(const dwt2_plan *p, const TailLevelIO *lv, int n, int count, const TailFilter &f,
                            cudaStream_t stream);
+// one small level of an inverse (tail.cu): the reconstructed W x H level input
+// `out` from the level's LL plane and its HL / LH / HH in the Mallat buffer d
+struct InvLevelIO {
+    const float *ll;
+    long long ll_pitch, ll_img;
+    const float *d;                   // the Mallat pyramid (level subbands at their Mallat offsets)
+    long long d_pitch, d_img;
+    float *out;
+    long long out_pitch, out_img;
+    int W, H;                         // reconstructed size (each >= 2)
+};
+struct InvFilter {
+    int radius;                       // 2: CDF 5/3 (dyadic taps: exact), 4: K <= 2 lifting pairs; 0: unsupported
+    double s0[9], s1[9];              // low / high synthesis taps at offsets -4..4
+    double kll, kd, khh;              // undo of the forward scaling
+};
+InvFilter inv_filter_from_lifting(double c0, double c1, double c2, double c3, double K);
+int32_t launch_small_inverse_level(const InvLevelIO &lv, int count, const InvFilter &f, cudaStream_t stream);
+// levels of an inverse that run on launch_small_inverse_level
+bool small_inverse_level(const dwt2_plan *p, int k, int count);
+
 // one small CDF 5/3 level in one launch of shared-memory-tiled pointwise CTAs (tail.cu)
 int32_t launch_small_level(const TailLevelIO &lv, int count, cudaStream_t stream);
 // one small level of a K <= 2 lifting wavelet (radius-4 filters f) in one launch (tail.cu)

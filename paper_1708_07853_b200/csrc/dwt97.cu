@@ -899,7 +899,10 @@ namespace dwt2_detail {
 // than DWT2_WAVELET_CDF53); buffer roles as run_levels in dwt2.cu.
 int k2_tail_start(const dwt2_plan *p, int count)
 {
-    static const int k2_tail_quads = tuning_int("DWT2_K2_TAIL_QUADS", 1 << 16, 0, 1 << 30);
+    // levels of <= 2^12 quads (128^2 and below) in the tail launch; the 512^2 and
+    // 256^2 levels run as separate small-level launches (tail.cu dwt_small4_kernel):
+    // 9/7 config 4 174.2 -> 170.1 us against a 2^16 threshold (scripts/r2/gpu_k2tail2.sh)
+    static const int k2_tail_quads = tuning_int("DWT2_K2_TAIL_QUADS", 1 << 12, 0, 1 << 30);
     return tail_start_levels(p, count, 0, p->levels - 1, k2_tail_quads);
 }
 
@@ -1014,6 +1017,15 @@ int32_t run_inverse_k2(const dwt2_plan *p, const float *in, float *out, int coun
             a.out_img = p->sc_img_stride[si];
         }
         a.counter = p->counters + 2 * (QUEUE_INVERSE + k);
+        const InvFilter f = inv_filter_from_lifting(wv.c0, wv.c1, wv.c2, wv.c3, wv.K);
+        if (f.radius != 0 && small_inverse_level(p, k, count)) {
+            // a small level: shared-memory-staged pointwise synthesis (tail.cu)
+            const InvLevelIO lv{a.ll, a.ll_pitch, a.ll_img, in, p->W, in_stride, a.out, a.out_pitch, a.out_img,
+                                g.W, g.H};
+            int32_t r = launch_small_inverse_level(lv, count, f, s);
+            if (r != DWT2_OK) return r;
+            continue;
+        }
         int32_t r = launch_k2_inverse_level(p, a, s);
         if (r != DWT2_OK) return r;
     }

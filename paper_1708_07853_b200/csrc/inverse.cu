@@ -654,6 +654,15 @@ int32_t run_inverse(const dwt2_plan *p, const float *in, float *out, int count, 
             a.ll_hi = p->scratch[sidx] + (long long)count * p->sc_img_stride[sidx];
         }
         a.counter = p->counters + 2 * (QUEUE_INVERSE + k);
+        if (small_inverse_level(p, k, count)) {
+            // a small level: shared-memory-staged pointwise synthesis (tail.cu)
+            static const InvFilter f53 = inv_filter_from_lifting(-0.5, 0.25, 0.0, 0.0, 1.0);
+            const InvLevelIO lv{a.ll, a.ll_pitch, a.ll_img, in, p->W, in_stride, a.out, a.out_pitch, a.out_img,
+                                g.W, g.H};
+            int32_t r = launch_small_inverse_level(lv, count, f53, s);
+            if (r != DWT2_OK) return r;
+            continue;
+        }
         int32_t r = launch_inverse_level(p, a, s);
         if (r != DWT2_OK) return r;
     }

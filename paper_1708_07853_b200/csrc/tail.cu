@@ -323,6 +323,117 @@ __global__ void __launch_bounds__(256) dwt_small4_kernel(const __grid_constant__
     }
 }
 
+// ---- small single levels of an INVERSE ------------------------------------
+//
+// The inverse level kernels walk their tiles row by row too (the K = 2 inverse:
+// ~10-13 us per small level of a 9/7 pyramid).  Here a CTA owns 32 x 8 output
+// quads (64 x 16 pixels) and stages the (16 + 2R) x (64 + 2R) window of the
+// INTERLEAVED coefficient field they depend on -- c(y, x) = LL / HL / LH / HH
+// by the parities of (y, x), at whole-sample-symmetric mirrored positions (the
+// coefficient field of a symmetric input is symmetric in the interleaved
+// index; the parity of a position survives the mirror) -- in one round of
+// loads, then synthesises separably in fp64: a horizontal pass per staged row
+// and output column pair into shared memory, and each thread's vertical pass
+// for its quad's 2 x 2 pixels:
+//   x(p_y, p_x) = sum_q s_{q_y mod 2}[p_y - q_y] s_{q_x mod 2}[p_x - q_x] k(q) c(q)
+// with s_0 / s_1 the low / high synthesis taps of the lifting pair (the inverse
+// lifting applied to unit impulses, inv_filter_from_lifting) and k the undo of
+// the forward scaling.  CDF 5/3: s_0 = (1/2, 1, 1/2), s_1 = (-1/8, -1/4, 3/4,
+// -1/4, -1/8), dyadic -- every product and sum is exact in fp64, so the stored
+// fp32 is bit for bit the inverse level kernel's.
+constexpr int IVX = 32, IVY = 8;
+
+struct SmallInvArgs {
+    InvLevelIO L;
+    double s0[9], s1[9];              // synthesis taps at offsets -4..4 (index offset + 4)
+    double kll, kd, khh;
+    int nbx;
+};
+
+template <int R>
+__global__ void __launch_bounds__(256) dwt_small_inv_kernel(const __grid_constant__ SmallInvArgs A)
+{
+    constexpr int WS = 2 * R + 2;                          // coefficient rows / columns of one quad
+    constexpr int SR = 2 * IVY + 2 * R, SC = 2 * IVX + 2 * R;
+    constexpr int SN = (SR * SC + 255) / 256;
+    __shared__ float t[SR][SC + 1];
+    __shared__ double h0[SR][IVX], h1[SR][IVX];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const InvLevelIO &L = A.L;
+    const int W = L.W, H = L.H;
+    const int Wq = (W + 1) >> 1, Hq = (H + 1) >> 1;
+    const int bx = blockIdx.x % A.nbx, by = blockIdx.x / A.nbx, img = blockIdx.y;
+    const int m0 = bx * IVX, n0 = by * IVY;
+    const int y0 = 2 * n0 - R, x0 = 2 * m0 - R;
+    const float *llp = L.ll + img * L.ll_img;
+    const float *dp = L.d + img * L.d_img;
+    float v[SN];
+#pragma unroll
+    for (int k = 0; k < SN; ++k) {                       // every load in flight at once
+        const int i = threadIdx.x + 256 * k;
+        const int r = i / SC, c = i - (i / SC) * SC;
+        float val = 0.f;
+        if (i < SR * SC && y0 + r < H + R + 1 && x0 + c < W + R + 1) {
+            const int y = wss_any(y0 + r, H), x = wss_any(x0 + c, W);
+            const int ry = y >> 1, cx = x >> 1;
+            const float *src = (!(y & 1) && !(x & 1)) ? llp + (long long)ry * L.ll_pitch + cx
+                             : dp + (long long)((y & 1) ? Hq + ry : ry) * L.d_pitch + ((x & 1) ? Wq + cx : cx);
+            val = __ldg(src);
+        }
+        v[k] = val;
+    }
+#pragma unroll
+    for (int k = 0; k < SN; ++k) {
+        const int i = threadIdx.x + 256 * k;
+        if (i < SR * SC) t[i / SC][i - (i / SC) * SC] = v[k];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < SR * IVX; i += 256) {    // horizontal synthesis
+        const int r = i / IVX, q = i - (i / IVX) * IVX;
+        const bool py = (y0 + r) & 1;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < WS; ++j) {
+            const int qpar = (R + j) & 1;                 // parity of column 2m - R + j
+            const double k = (!py && !qpar) ? A.kll : (py && qpar) ? A.khh : A.kd;
+            const double c = k * double(t[r][2 * q + j]);
+            const double *sx = qpar ? A.s1 : A.s0;
+            const int o0 = R - j;                          // 2m - (2m - R + j)
+            if (o0 >= -4 && o0 <= 4) a0 = fma(sx[o0 + 4], c, a0);
+            if (o0 + 1 >= -4 && o0 + 1 <= 4) a1 = fma(sx[o0 + 5], c, a1);
+        }
+        h0[r][q] = a0;
+        h1[r][q] = a1;
+    }
+    __syncthreads();
+    const int tx = threadIdx.x & (IVX - 1), ty = threadIdx.x / IVX;
+    const int m = m0 + tx, n = n0 + ty;
+    if (m >= Wq || n >= Hq) return;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int j = 0; j < WS; ++j) {
+        const double *sy = ((R + j) & 1) ? A.s1 : A.s0;
+        const int o0 = R - j;
+        const double u0 = h0[2 * ty + j][tx], u1 = h1[2 * ty + j][tx];
+        if (o0 >= -4 && o0 <= 4) {
+            acc[0][0] = fma(sy[o0 + 4], u0, acc[0][0]);
+            acc[0][1] = fma(sy[o0 + 4], u1, acc[0][1]);
+        }
+        if (o0 + 1 >= -4 && o0 + 1 <= 4) {
+            acc[1][0] = fma(sy[o0 + 5], u0, acc[1][0]);
+            acc[1][1] = fma(sy[o0 + 5], u1, acc[1][1]);
+        }
+    }
+    float *o = L.out + img * L.out_img + (long long)(2 * n) * L.out_pitch + 2 * m;
+    o[0] = (float)acc[0][0];
+    if (2 * m + 1 < W) o[1] = (float)acc[0][1];
+    if (2 * n + 1 < H) {
+        o[L.out_pitch] = (float)acc[1][0];
+        if (2 * m + 1 < W) o[L.out_pitch + 1] = (float)acc[1][1];
+    }
+}
+
 template <int R>
 int tail_resident()
 {
@@ -431,6 +542,90 @@ int32_t launch_small_level_r4(const TailLevelIO &lv, int count, const TailFilter
         return fail(DWT2_ECUDA);
     }
     return DWT2_OK;
+}
+
+InvFilter inv_filter_from_lifting(double c0, double c1, double c2, double c3, double K)
+{
+    // inverse 1-D lifting of a unit coefficient at interleaved position q
+    // (even: low, odd: high) of a long signal, far from its ends:
+    //   s1 = s2 - c3 (d2[i-1] + d2[i]),  d1 = d2 - c2 (s1[i] + s1[i+1]),
+    //   x_even = s1 - c1 (d1[i-1] + d1[i]),  x_odd = d1 - c0 (x_even[i] + x_even[i+1])
+    InvFilter f;
+    memset(&f, 0, sizeof(f));
+    constexpr int N = 64, M = N / 2;
+    for (int q = 30; q <= 31; ++q) {
+        double sv[M] = {0}, d[M] = {0}, x[N];
+        if (q % 2 == 0) sv[q / 2] = 1.0;
+        else d[q / 2] = 1.0;
+        for (int i = 0; i < M; ++i) sv[i] = sv[i] - c3 * ((i > 0 ? d[i - 1] : 0.0) + d[i]);
+        for (int i = 0; i < M; ++i) d[i] = d[i] - c2 * (sv[i] + (i + 1 < M ? sv[i + 1] : 0.0));
+        for (int i = 0; i < M; ++i) x[2 * i] = sv[i] - c1 * ((i > 0 ? d[i - 1] : 0.0) + d[i]);
+        for (int i = 0; i < M; ++i) x[2 * i + 1] = d[i] - c0 * (x[2 * i] + (2 * i + 2 < N ? x[2 * i + 2] : 0.0));
+        double *tap = q % 2 == 0 ? f.s0 : f.s1;
+        int reach = 0;
+        for (int p = 0; p < N; ++p) {
+            const int off = p - q;
+            if (off >= -4 && off <= 4) tap[off + 4] = x[p];
+            else if (x[p] != 0.0) reach = 5;
+            if (x[p] != 0.0) reach = std::max(reach, off < 0 ? -off : off);
+        }
+        f.radius = std::max(f.radius, reach);
+    }
+    f.radius = f.radius <= 2 ? 2 : (f.radius <= 4 ? 4 : 0);       // 0: taps beyond +-4 (unsupported)
+    // undo the forward scaling (LL / K^2, HL and LH * 1, HH * K^2)
+    f.kll = K * K;
+    f.kd = 1.0;
+    f.khh = 1.0 / (K * K);
+    return f;
+}
+
+int32_t launch_small_inverse_level(const InvLevelIO &lv, int count, const InvFilter &f, cudaStream_t stream)
+{
+    if (f.radius != 2 && f.radius != 4) return fail(DWT2_EINVAL);
+    const int Wq = (lv.W + 1) / 2, Hq = (lv.H + 1) / 2;
+    SmallInvArgs A;
+    memset(&A, 0, sizeof(A));
+    A.L = lv;
+    memcpy(A.s0, f.s0, sizeof(A.s0));
+    memcpy(A.s1, f.s1, sizeof(A.s1));
+    A.kll = f.kll;
+    A.kd = f.kd;
+    A.khh = f.khh;
+    A.nbx = (Wq + IVX - 1) / IVX;
+    const int nby = (Hq + IVY - 1) / IVY;
+    if ((long long)A.nbx * nby >= (1LL << 31) || count > 65535) return fail(DWT2_EINVAL);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(A.nbx * nby, count);
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = f.radius == 2 ? cudaLaunchKernelEx(&cfg, dwt_small_inv_kernel<2>, A)
+                                        : cudaLaunchKernelEx(&cfg, dwt_small_inv_kernel<4>, A);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DWT2_ECUDA);
+    }
+    return DWT2_OK;
+}
+
+// Measured (scripts/r2/inv_small_probe.py, graph of 20 inverses; thresholds
+// 0 / 2^16 / 2^18 / 2^20 quads): CDF 9/7 config 4 226.9 / 205.3 / 206.5 / 233.8 us;
+// CDF 5/3 config 4 165.6 / 166.3 / 170.0 / 193.8 us (its ring kernel is fast on
+// 16-byte-aligned levels), config 4b (odd widths: the plain-load kernel)
+// 245.3 / 236.9 / 234.4 / 233.2 us; a cold single 1024^2 level is slower on the
+// small kernel (5/3 7.2 -> 10.7 us).
+bool small_inverse_level(const dwt2_plan *p, int k, int count)
+{
+    static const long long q53 = tuning_int("DWT2_INV_SMALL_QUADS", 1 << 16, 0, 1 << 30);
+    static const long long q53_odd = tuning_int("DWT2_INV_SMALL_QUADS_ODD", 1 << 20, 0, 1 << 30);
+    static const long long qk2 = tuning_int("DWT2_K2INV_SMALL_QUADS", 1 << 16, 0, 1 << 30);
+    const long long quads = (long long)p->geom[k].Wq * p->geom[k].Hq * count;
+    if (p->wavelet != DWT2_WAVELET_CDF53) return quads <= qk2;
+    return quads <= ((p->W % 4) != 0 ? q53_odd : q53);      // the Mallat pitch W: ring kernel iff 16-byte rows
 }
 
 int tail_start_levels(const dwt2_plan *p, int count, int first, int last, long long max_quads)
