@@ -1669,7 +1669,8 @@ bool small_level(const dwt2_plan *p, int k, int count)
 {
     static const long long small_first = tuning_int("DWT2_SMALL_QUADS", 1 << 16, 0, 1 << 30);
     static const long long small_ll = tuning_int("DWT2_SMALL_QUADS_LL", 1 << 18, 0, 1 << 30);
-    return (long long)p->geom[k].Wq * p->geom[k].Hq * count <= (k == 0 ? small_first : small_ll);
+    return count <= 65535 &&          // images go to gridDim.y
+           (long long)p->geom[k].Wq * p->geom[k].Hq * count <= (k == 0 ? small_first : small_ll);
 }
 
 // Forward of levels [first, last] for `count` images.  Level 1 reads `in`.

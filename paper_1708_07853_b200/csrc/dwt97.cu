@@ -958,7 +958,7 @@ int32_t run_levels_k2(const dwt2_plan *p, const float *in, float *out, int count
         }
         // small levels: one launch of shared-memory-staged CTAs (tail.cu)
         static const long long k2_small = tuning_int("DWT2_K2_SMALL_QUADS", 1 << 18, 0, 1 << 30);
-        if ((long long)g.Wq * g.Hq * count <= k2_small) {
+        if (count <= 65535 && (long long)g.Wq * g.Hq * count <= k2_small) {
             const TailLevelIO lv{a.in, a.in_pitch, a.in_img, a.ll, a.ll_pitch, a.ll_img,
                                  out, a.out_pitch, a.out_img, a.W, a.H};
             int32_t r = launch_small_level_r4(lv, count, tail_filter_from_lifting(wv.c0, wv.c1, wv.c2, wv.c3, wv.K), s);

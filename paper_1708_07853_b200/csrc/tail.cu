@@ -624,6 +624,7 @@ bool small_inverse_level(const dwt2_plan *p, int k, int count)
     static const long long q53_odd = tuning_int("DWT2_INV_SMALL_QUADS_ODD", 1 << 20, 0, 1 << 30);
     static const long long qk2 = tuning_int("DWT2_K2INV_SMALL_QUADS", 1 << 16, 0, 1 << 30);
     const long long quads = (long long)p->geom[k].Wq * p->geom[k].Hq * count;
+    if (count > 65535) return false;                         // images go to gridDim.y
     if (p->wavelet != DWT2_WAVELET_CDF53) return quads <= qk2;
     return quads <= ((p->W % 4) != 0 ? q53_odd : q53);      // the Mallat pitch W: ring kernel iff 16-byte rows
 }
