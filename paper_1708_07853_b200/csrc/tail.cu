@@ -248,8 +248,8 @@ __global__ void __launch_bounds__(256) dwt53_small_kernel(const __grid_constant_
 // below it.  Measured (scripts/r2/k2small_probe.py): a 1024^2 9/7 level 9.53 ->
 // 8.72 us, the 9/7 config-4 pyramid 175.6 -> 174.4 us; from 2048^2 up it loses
 // (15.2 -> 29.0 us: shared-memory and fp64 issue bound; staging the tile as fp64
-// to save the conversions was slower still, 43 us: 16-byte-strided reads), so
-// levels of <= 2^18 quads only.
+// to save the conversions was slower still, 43 us with 16-byte-strided reads and
+// 41.8 us with even / odd columns apart), so levels of <= 2^18 quads only.
 constexpr int R4X = 32, R4Y = 8;
 constexpr int R4R = 2 * R4Y + 7, R4C = 2 * R4X + 7;      // staged rows / columns
 constexpr int R4N = (R4R * R4C + 255) / 256;
