@@ -35,3 +35,28 @@ def test_c_example_runs(tmp_path, W, H, L):
     res = subprocess.run([exe, str(W), str(H), str(L)], capture_output=True, text=True, timeout=120)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "max |detail| 0," in res.stdout
+
+
+def build_peer_example(tmp_path):
+    _build.build()
+    exe = str(tmp_path / "peer_strips_c")
+    cmd = ["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "examples", "peer_strips_c.c"), "-L", PKG, "-ldwt2", "-L", "/usr/local/cuda/lib64",
+           "-lcudart", f"-Wl,-rpath,{PKG}", "-o", exe]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    assert res.returncode == 0, res.stdout + res.stderr
+    return exe
+
+
+def test_c_peer_example_builds(tmp_path):
+    """The peer-strip entry points from plain C (examples/peer_strips_c.c)."""
+    assert os.path.exists(build_peer_example(tmp_path))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W,H,L,G", [(1000, 1024, 3, 4), (777, 513, 2, 3), (4096, 4096, 6, 8)])
+def test_c_peer_example_runs(tmp_path, W, H, L, G):
+    exe = build_peer_example(tmp_path)
+    res = subprocess.run([exe, str(W), str(H), str(L), str(G)], capture_output=True, text=True, timeout=120)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "single-image transform 0" in res.stdout
