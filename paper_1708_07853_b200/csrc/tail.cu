@@ -181,7 +181,9 @@ __global__ void __launch_bounds__(TAIL_THREADS) dwt_tail_kernel(const __grid_con
 // 2 m0 - 2 .. 2 m0 + 64, whole-sample symmetric at the image edges) into
 // shared memory in ONE round of independent coalesced loads, and every thread
 // evaluates one quad pointwise with the exact 5 x 5 analysis filters of the
-// radius-2 tail path (bit for bit the level kernel's values).
+// radius-2 tail path (bit for bit the level kernel's values).  (Staging even
+// and odd columns apart to avoid the 2-way bank conflicts of the window reads
+// measured slower: 512^2 3.7 -> 4.1 us.)
 constexpr int SQX = 32, SQY = 8;                         // quads per CTA
 constexpr int STR = 2 * SQY + 3, STC = 2 * SQX + 3;      // staged rows / columns
 constexpr int SN = (STR * STC + 255) / 256;              // staged floats per thread
