@@ -287,7 +287,10 @@ class OursRunner:
             img = g.image(0)
             self.sha.update(img.tobytes())
             if self.exchange == "peer":
-                self.ex = D.PeerStripPyramid(g.width, g.height, rank, world, cfg.levels, device=device)
+                # flag waits take microseconds; a 2 s bound turns a broken mapping into a
+                # quick failure (checked after the warm-up) instead of a long hang
+                self.ex = D.PeerStripPyramid(g.width, g.height, rank, world, cfg.levels, device=device,
+                                             timeout_ms=2000)
                 try:
                     self.ex.connect()          # all_gather of the CUDA IPC descriptors (once)
                     ok = 1
@@ -913,6 +916,16 @@ def main():
     for _ in range(max(3, args.warmup)):
         runner.step()
     torch.cuda.synchronize()
+    if runner.mode == "strip" and OursRunner.exchange == "peer":
+        # a timed-out flag wait on any rank (DWT2_ETIMEOUT): no timing of a broken exchange
+        bad = torch.tensor([0 if runner.ex.status() == 0 else 1], device=device)
+        if world > 1:
+            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        if int(bad.item()):
+            if rank == 0:
+                print(json.dumps({"metric": metric_name(args), "error": "peer halo exchange timed out during "
+                                  "the warm-up (DWT2_ETIMEOUT): no timing is reported"}), flush=True)
+            raise SystemExit(3)
     graph = None
     if not args.no_graph and (runner.mode != "strip" or OursRunner.exchange == "peer"):
         # the K timed steps as ONE CUDA graph (the level kernels keep their
