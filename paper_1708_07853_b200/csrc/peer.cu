@@ -21,7 +21,6 @@
 
 #include <algorithm>
 #include <cstring>
-#include <mutex>
 
 #include "dwt2_internal.h"
 
