@@ -1129,6 +1129,13 @@ KernelFn kernel_peer(bool large, bool vec)
     return vec ? dwt53_level_kernel<true, true, AR_GROUPED, 1, S, true> : dwt53_level_kernel<true, false, AR_GROUPED, 1, S, true>;
 }
 
+// the 3-stage row-grouped kernel of large levels with pitches that are not a multiple of 16 bytes
+KernelFn kernel_large_grp(bool vec, int gg)
+{
+    if (gg == 2) return vec ? dwt53_level_kernel<true, true, AR_GROUPED, 2, S_LARGE> : dwt53_level_kernel<true, false, AR_GROUPED, 2, S_LARGE>;
+    return vec ? dwt53_level_kernel<true, true, AR_GROUPED, 4, S_LARGE> : dwt53_level_kernel<true, false, AR_GROUPED, 4, S_LARGE>;
+}
+
 KernelFn kernel_large(bool vec)
 {
     return vec ? dwt53_level_kernel<true, true, AR_GROUPED, 1, S_LARGE> : dwt53_level_kernel<true, false, AR_GROUPED, 1, S_LARGE>;
@@ -1310,6 +1317,8 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     const bool large = pol.tb_large > 0 && slab_rows >= (long long)pol.large_tpw * pol.tb_large * warps_full;
     static const int use_s3 = tuning_int("DWT2_LARGE_S3", 1, 0, 1);
     const bool s3 = use_s3 && large && tma && ar == AR_GROUPED;      // the 3-stage kernel (S_LARGE)
+    static const int use_s3g = tuning_int("DWT2_LARGE_S3G", 1, 0, 1);
+    const bool s3g = use_s3 && use_s3g && large && grp && ar == AR_GROUPED && p->max_ctas[3] > 0;   // its GRP form
     if (large) {
         // large levels (>= large_tpw tiles per warp at tb_large quad rows):
         // tb_large, measured best from 16384 x 6144 up -- 16384 x 8192 (a
@@ -1363,7 +1372,8 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     a.fd_slabs = make_fastdiv(unsigned(a.nslabs));
     a.fd_img = make_fastdiv(unsigned(a.nblk * a.nslabs));
     const long long want_ctas = (ntiles + WARPS - 1) / WARPS;
-    const int grid = int(std::max<long long>(1, std::min<long long>(s3 ? p->max_ctas[2] : max_ctas, want_ctas)));
+    const int grid = int(std::max<long long>(1, std::min<long long>(s3 ? p->max_ctas[2] : s3g ? p->max_ctas[3] : max_ctas,
+                                                                    want_ctas)));
     a.nwarps = grid * WARPS;
     a.static_tiles = ntiles <= a.nwarps ? 1 : 0;
     // the first stage of a tile on the unrolled path: measured faster on
@@ -1387,14 +1397,16 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid + a.pb_ctas);
     cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = grp ? RingG<true, 2>::SMEM : s3 ? Ring<true, S_LARGE>::SMEM : tma ? Ring<true>::SMEM : Ring<false>::SMEM;
+    cfg.dynamicSmemBytes = grp ? (s3g ? RingG<true, 2, S_LARGE>::SMEM : RingG<true, 2>::SMEM)
+                               : s3 ? Ring<true, S_LARGE>::SMEM : tma ? Ring<true>::SMEM : Ring<false>::SMEM;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    KernelFn fn = s3 ? kernel_large(vec) : kernel_for(tma || grp, vec, ar, grp ? 1 << glog : 1);
+    KernelFn fn = s3 ? kernel_large(vec) : s3g ? kernel_large_grp(vec, 1 << glog)
+                                          : kernel_for(tma || grp, vec, ar, grp ? 1 << glog : 1);
     if (io.peer) {
         if (!tma || ar != AR_GROUPED) return fail(DWT2_EINVAL);        // peer.cu buffers are TMA-aligned
         fn = kernel_peer(s3, vec);
@@ -1409,7 +1421,7 @@ int32_t launch_level(const dwt2_plan *p, int level, int W, int H, const LaunchIO
 
 int32_t configure_kernels(int *max_ctas)
 {
-    static int cached[3] = {0, 0, 0};
+    static int cached[4] = {0, 0, 0, 0};
     static std::once_flag once;
     static int32_t status = DWT2_OK;
     std::call_once(once, [] {
@@ -1468,11 +1480,24 @@ int32_t configure_kernels(int *max_ctas)
             return;
         }
         cached[2] = sms * per_sm;
+        for (int v = 0; v < 4; ++v)
+            if (cudaFuncSetAttribute(kernel_large_grp((v & 1) == 0, v < 2 ? 2 : 4), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(RingG<true, 2, S_LARGE>::SMEM)) != cudaSuccess) {
+                status = DWT2_ECUDA;
+                return;
+            }
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_large_grp(true, 4), THREADS,
+                                                          RingG<true, 2, S_LARGE>::SMEM) != cudaSuccess || per_sm < 1) {
+            status = DWT2_ECUDA;
+            return;
+        }
+        cached[3] = sms * per_sm;
     });
     cudaGetLastError();
     max_ctas[0] = cached[0];
     max_ctas[1] = cached[1];
     max_ctas[2] = cached[2];
+    max_ctas[3] = cached[3];
     return status;
 }
 

@@ -106,7 +106,8 @@ struct dwt2_plan {
     float *scratch[2];
     long long sc_pitch[2], sc_img_stride[2];
     size_t scratch_bytes;
-    int max_ctas[3];          // resident CTAs of the forward kernels: [0] cp.async, [1] TMA, [2] TMA 3-stage (large levels)
+    int max_ctas[4];          // resident CTAs of the forward kernels: [0] cp.async, [1] TMA, [2] TMA 3-stage (large
+                              // levels), [3] row-grouped TMA 3-stage (large levels of pitches not a multiple of 16 B)
     int sms;                  // multiprocessors of the plan's device
     unsigned int *counters;   // per level: tile queue + finished-warp counter (device, self-resetting)
     // host-side caches (the API serialises calls on one plan)
