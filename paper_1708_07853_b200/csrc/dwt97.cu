@@ -264,10 +264,9 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
     float *chl = a.hl + ob0, *clh = a.lh + ob0, *chh = a.hh + ob0;
     // rows in groups of D so that every ring slot index is a compile-time
     // constant (a dynamic index would force the prefetched loads to land)
-    for (int rb = r_first; rb <= r_last; rb += D) {
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        const int r = rb + j;
+    // one walk row: ring slot j (compile-time), walk row r, warm-up phase ph
+    // (r - r_first while < 4, else 4; a compile-time constant at every call)
+    auto row = [&](const int j, const int r, const int ph) {
         RawRow R;
         if (ASYNC) {
             cp_async_wait<D - 1>();                    // row r's group (the oldest) has landed
@@ -293,13 +292,23 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
         k2r hl1[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) hl1[i] = fma(k2r(a.c0), av[i] + K2_RIGHT(av, i, a_nb), bv[i]);
+        // warm-up: the first 4 rows of a tile only build the carries that
+        // output row n0 needs, so step s runs from walk row r_first + s on
+        // (1: predict-1 completion + LH1, 2: HL1 / LL1 / HL'2, 3: predict-2
+        // completion + LH2, 4: HL2 / LL2).  The skipped values feed nothing
+        // that is stored; the branch is warp-uniform.
+        k2r lh1[QK], hh1[QK], C1[QK], A1[QK], B1[QK], hl2[QK], lh2[QK], hh2[QK], C2[QK];
+#pragma unroll
+        for (int i = 0; i < QK; ++i) {
+            lh1[i] = hh1[i] = C1[i] = A1[i] = B1[i] = hl2[i] = lh2[i] = hh2[i] = C2[i] = k2r(0);
+        }
+        if (ph >= 1) {
         // ---- predict 1 completes row r-1: LH'1 = c + c0 (a + a[n+1]),
         //      HH'1 = d + c0 (c + c[m+1]) + c0 (HL'1 + HL'1[n+1])
         k2r cp_[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) cp_[i] = cy[i].c;
         const k2r c_nb = shr(cp_[0]);
-        k2r lh1[QK], hh1[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) {
             lh1[i] = fma(k2r(a.c0), cy[i].a + av[i], cy[i].c);
@@ -308,52 +317,58 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
         // ---- update 1, row r-1: LH1 = LH'1 + c1 (HH'1 + HH'1[m-1]),
         //      HL1 = HL'1 + c1 (HH'1 + HH'1[n-1]),
         //      LL1 = a + c1 (HL'1 + HL'1[m-1]) + c1 (LH1 + LH1[n-1])
+        const k2r hh1_l = shl(hh1[QK - 1]);
+#pragma unroll
+        for (int i = 0; i < QK; ++i) C1[i] = fma(k2r(a.c1), hh1[i] + K2_LEFT(hh1, i, hh1_l), lh1[i]);
+        }
+        if (ph >= 2) {
         k2r hlp[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) hlp[i] = cy[i].hl1;
-        const k2r hh1_l = shl(hh1[QK - 1]);
         const k2r hl1p_l = shl(hlp[QK - 1]);
-        k2r A1[QK], B1[QK], C1[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) {
-            C1[i] = fma(k2r(a.c1), hh1[i] + K2_LEFT(hh1, i, hh1_l), lh1[i]);
             B1[i] = fma(k2r(a.c1), hh1[i] + cy[i].hh1, cy[i].hl1);
             A1[i] = fma(k2r(a.c1), C1[i] + cy[i].lh1f, fma(k2r(a.c1), cy[i].hl1 + K2_LEFT(hlp, i, hl1p_l), cy[i].a));
         }
         // ---- predict 2 on the update-1 output, row r-1 (same-row part):
         //      HL'2 = HL1 + c2 (LL1 + LL1[m+1])
         const k2r A_nb = shr(A1[0]);
-        k2r hl2[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) hl2[i] = fma(k2r(a.c2), A1[i] + K2_RIGHT(A1, i, A_nb), B1[i]);
+        }
+        if (ph >= 3) {
         // ---- predict 2 completes row r-2 (carried A, LH1 = lh1f, HH1 = hh1, HL'2):
         //      LH'2 = LH1 + c2 (LL1 + LL1[n+1]), HH'2 = HH1 + c2 (LH1 + LH1[m+1]) + c2 (HL'2 + HL'2[n+1])
         k2r lf[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) lf[i] = cy[i].lh1f;
         const k2r C_nb = shr(lf[0]);
-        k2r lh2[QK], hh2[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) {
             lh2[i] = fma(k2r(a.c2), cy[i].A + A1[i], cy[i].lh1f);
             hh2[i] = fma(k2r(a.c2), cy[i].hl2 + hl2[i], fma(k2r(a.c2), cy[i].lh1f + K2_RIGHT(lf, i, C_nb), cy[i].hh1));
         }
         // ---- update 2, row r-2
+        const k2r hh2_l = shl(hh2[QK - 1]);
+#pragma unroll
+        for (int i = 0; i < QK; ++i) C2[i] = fma(k2r(a.c3), hh2[i] + K2_LEFT(hh2, i, hh2_l), lh2[i]);
+        }
+        k2r A2[QK], B2[QK];
+        if (ph >= 4) {
         k2r h2p[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) h2p[i] = cy[i].hl2;
-        const k2r hh2_l = shl(hh2[QK - 1]);
         const k2r hl2p_l = shl(h2p[QK - 1]);
-        k2r A2[QK], B2[QK], C2[QK];
 #pragma unroll
         for (int i = 0; i < QK; ++i) {
-            C2[i] = fma(k2r(a.c3), hh2[i] + K2_LEFT(hh2, i, hh2_l), lh2[i]);
             B2[i] = fma(k2r(a.c3), hh2[i] + cy[i].hh2, cy[i].hl2);
             A2[i] = fma(k2r(a.c3), C2[i] + cy[i].lh2f, fma(k2r(a.c3), cy[i].hl2 + K2_LEFT(h2p, i, hl2p_l), cy[i].A));
         }
-        // ---- store output row r-2 (scaled)
+        }
+        // ---- store output row r-2 (scaled); ph < 4 only on warm-up rows (n < n0)
         const int n = r - 2;
-        if (n >= n0 && n < n1 && out_lane) {
+        if (ph >= 4 && n >= n0 && n < n1 && out_lane) {
             float oLL[QK], oHL[QK], oLH[QK], oHH[QK];
 #pragma unroll
             for (int i = 0; i < QK; ++i) {
@@ -414,10 +429,35 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
         }
         if (ASYNC) {
             // slot j is free again (its row was consumed above)
-            if (rb + D <= r_last) issue(j, r + D);       // the next group exists
+            if (r - j + D <= r_last) issue(j, r + D);    // the next group exists
             cp_async_commit();
         }
-    }
+    };
+    if (VEC) {
+        // 16-byte rows (the ring path and its edge slabs): every row runs every
+        // step.  Peeling the warm-up group measured slower here (8192^2 9/7
+        // 389 -> 378 Gpix/s, 16384^2 unchanged: the extra copy of the D-row
+        // body costs instruction-cache misses), and so did peeling only the
+        // edge slabs' register path inside this kernel (config 4 389.6 -> 384.8)
+        for (int rb = r_first; rb <= r_last; rb += D) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) row(j, rb + j, 4);
+        }
+    } else {
+        // unaligned rows (the register path on every slab): the warm-up rows
+        // are peeled, their skipped steps fold away at compile time and the
+        // steady-state body carries no phase test (a run-time phase test cost
+        // 2-6 %; peeled: config 4b 9/7 287.3 -> 296.1 Gpix/s)
+        constexpr int PEEL = (4 + D - 1) / D;
+#pragma unroll
+        for (int g = 0; g < PEEL; ++g) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) row(j, r_first + g * D + j, g * D + j < 4 ? g * D + j : 4);
+        }
+        for (int rb = r_first + PEEL * D; rb <= r_last; rb += D) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) row(j, rb + j, 4);
+        }
     }
     if (ASYNC) cp_async_wait<0>();
 }
@@ -660,10 +700,9 @@ __device__ void kinv_tile(const K2InvArgs &a, float *ring, int img, int m0, int 
         issue(j, r_first + j);
         if (ASYNC) cp_async_commit();
     }
-    for (int rb = r_first; rb <= r_last; rb += D) {
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        const int n = rb + j;
+    // one walk row: ring slot j (compile-time), quad row n, warm-up phase ph
+    // (n - r_first while < 4, else 4; a compile-time constant at every call)
+    auto row = [&](const int j, const int n, const int ph) {
         InvRaw R;
         if (ASYNC) {
             cp_async_wait<D - 1>();
@@ -702,54 +741,61 @@ __device__ void kinv_tile(const K2InvArgs &a, float *ring, int img, int m0, int 
 #pragma unroll
         for (int i = 0; i < 2; ++i)
             ll1[i] = fma(-k2r(a.c3), LH[i] + cy[i].lh, fma(-k2r(a.c3), hl2p[i] + (i == 0 ? hl2p_l : hl2p[0]), a2[i]));
-        // ---- undo P2 completes row n-1 (carried hl2p, lh2p, ll1, hh2 of row n-1)
-        k2r pll1[2];
+        // warm-up: the first 4 rows of a tile only build the carries that
+        // output quad row n0 needs, so undo-P2 runs from walk row r_first + 2
+        // on, undo-U1 from r_first + 3 and undo-P1 (the output) from r_first + 4;
+        // the skipped values feed nothing that is stored (warp-uniform branches)
+        k2r pll1[2], hl1[2], lh1[2], hh1[2], lh1p[2], hl1p[2], av[2];
 #pragma unroll
-        for (int i = 0; i < 2; ++i) pll1[i] = cy[i].ll1;
+        for (int i = 0; i < 2; ++i) {
+            pll1[i] = cy[i].ll1;
+            hl1[i] = lh1[i] = hh1[i] = lh1p[i] = hl1p[i] = av[i] = k2r(0);
+        }
+        if (ph >= 2) {
+        // ---- undo P2 completes row n-1 (carried hl2p, lh2p, ll1, hh2 of row n-1)
         const k2r ll1_r = shr(pll1[0]);
-        k2r hl1[2], lh1[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             hl1[i] = fma(-k2r(a.c2), pll1[i] + (i == 0 ? pll1[1] : ll1_r), cy[i].hl2p);
             lh1[i] = fma(-k2r(a.c2), pll1[i] + ll1[i], cy[i].lh2p);
         }
         const k2r lh1_r = shr(lh1[0]);
-        k2r hh1[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
             hh1[i] = fma(-k2r(a.c2), cy[i].hl2p + hl2p[i], fma(-k2r(a.c2), lh1[i] + (i == 0 ? lh1[1] : lh1_r), cy[i].hh2));
+        }
+        if (ph >= 3) {
         // ---- undo U1, row n-1 (carried hh1, lh1 of row n-2)
         const k2r hh1_l = shl(hh1[1]);
-        k2r lh1p[2], hl1p[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             lh1p[i] = fma(-k2r(a.c1), hh1[i] + (i == 0 ? hh1_l : hh1[0]), lh1[i]);
             hl1p[i] = fma(-k2r(a.c1), hh1[i] + cy[i].hh1, hl1[i]);
         }
         const k2r hl1p_l = shl(hl1p[1]);
-        k2r av[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
             av[i] = fma(-k2r(a.c1), lh1[i] + cy[i].lh1, fma(-k2r(a.c1), hl1p[i] + (i == 0 ? hl1p_l : hl1p[0]), pll1[i]));
+        }
+        k2r pa[2], bo[2], co[2], dout[2];
+        if (ph >= 4) {
         // ---- undo P1 completes row n-2 (carried a, hl1p, lh1p, hh1 of row n-2)
-        k2r pa[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) pa[i] = cy[i].a;
         const k2r a_r = shr(pa[0]);
-        k2r bo[2], co[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             bo[i] = fma(-k2r(a.c0), pa[i] + (i == 0 ? pa[1] : a_r), cy[i].hl1p);
             co[i] = fma(-k2r(a.c0), pa[i] + av[i], cy[i].lh1p);
         }
         const k2r c_r = shr(co[0]);
-        k2r dout[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
             dout[i] = fma(-k2r(a.c0), cy[i].hl1p + hl1p[i], fma(-k2r(a.c0), co[i] + (i == 0 ? co[1] : c_r), cy[i].hh1));
-        // ---- store pixel rows 2(n-2), 2(n-2)+1
+        }
+        // ---- store pixel rows 2(n-2), 2(n-2)+1 (ph < 4 only on warm-up rows, q < n0)
         const int q = n - 2;
-        if (q >= n0 && q < n1 && out_lane) {
+        if (ph >= 4 && q >= n0 && q < n1 && out_lane) {
             const int x = 2 * mo, y = 2 * q;
             float *r0 = a.out + (long long)img * a.out_img + (long long)y * a.out_pitch + x;
             float *r1 = r0 + a.out_pitch;
@@ -784,10 +830,31 @@ __device__ void kinv_tile(const K2InvArgs &a, float *ring, int img, int m0, int 
             cy[i].ll1 = ll1[i];
         }
         if (ASYNC) {
-            if (rb + D <= r_last) issue(j, n + D);     // slot j's row was consumed above
+            if (n - j + D <= r_last) issue(j, n + D);  // slot j's row was consumed above
             cp_async_commit();
         }
-    }
+    };
+    if (ASYNC) {
+        // every row runs every step (gating the warm-up rows at run time
+        // measured neutral on the ring path: 9/7 inverse config 3 / 4 within 0.3 %)
+        for (int rb = r_first; rb <= r_last; rb += D) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) row(j, rb + j, 4);
+        }
+    } else {
+        // register path (edge slabs, unaligned planes): the warm-up rows are
+        // peeled and their skipped steps fold away at compile time (9/7
+        // inverse config 4 325.5 -> 332.9 Gpix/s, 4b 240.0 -> 244.8, 3 691.5 -> 696.0)
+        constexpr int PEEL = (4 + D - 1) / D;
+#pragma unroll
+        for (int g = 0; g < PEEL; ++g) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) row(j, r_first + g * D + j, g * D + j < 4 ? g * D + j : 4);
+        }
+        for (int rb = r_first + PEEL * D; rb <= r_last; rb += D) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) row(j, rb + j, 4);
+        }
     }
     if (ASYNC) cp_async_wait<0>();
 }
