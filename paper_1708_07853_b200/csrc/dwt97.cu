@@ -58,6 +58,9 @@ constexpr int RW = 2 * SLABQ;              // floats per staged pixel row (= 64 
 #define DWT2_K2_DS 5                      // measured: 5 > 4 > 6 > 8 > 2 (the row loop is unrolled DS times: i-cache)
 #endif
 constexpr int DS = DWT2_K2_DS;             // raw quad rows in flight per warp (shared-memory ring, cp.async)
+#ifndef DWT2_K2_PEEL_ALL
+#define DWT2_K2_PEEL_ALL 0                 // measurement builds: peel the warm-up rows on the ring path too
+#endif
 #ifndef DWT2_K2_DR
 #define DWT2_K2_DR 1
 #endif
@@ -433,7 +436,7 @@ __device__ void k2_tile(const K2Args &a, float *wring, int img, int m0, int n0, 
             cp_async_commit();
         }
     };
-    if (VEC) {
+    if (VEC && !DWT2_K2_PEEL_ALL) {
         // 16-byte rows (the ring path and its edge slabs): every row runs every
         // step.  Peeling the warm-up group measured slower here (8192^2 9/7
         // 389 -> 378 Gpix/s, 16384^2 unchanged: the extra copy of the D-row
@@ -662,6 +665,9 @@ __device__ __forceinline__ void cp_async8(float *dst, const float *src)
                  "l"(src) : "memory");
 }
 
+#ifndef DWT2_K2INV_PEEL_ALL
+#define DWT2_K2INV_PEEL_ALL 0              // measurement builds: peel the warm-up rows on the ring path too
+#endif
 #ifndef DWT2_K2INV_DS
 #define DWT2_K2INV_DS 4
 #endif
@@ -834,7 +840,7 @@ __device__ void kinv_tile(const K2InvArgs &a, float *ring, int img, int m0, int 
             cp_async_commit();
         }
     };
-    if (ASYNC) {
+    if (ASYNC && !DWT2_K2INV_PEEL_ALL) {
         // every row runs every step (gating the warm-up rows at run time
         // measured neutral on the ring path: 9/7 inverse config 3 / 4 within 0.3 %)
         for (int rb = r_first; rb <= r_last; rb += D) {
